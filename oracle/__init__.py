@@ -1,0 +1,148 @@
+"""CPU oracle for the LiNR pre-filtered top-K scan — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference legs) may
+import this package. The product path (paper_2407_13218_b200) never imports it and shares no
+code with it. See linr_oracle.cpp for the definition and the PAPER.md passages it follows.
+
+Parity status: every function is pinned in tests/test_oracle.py against values fixed by the
+paper's semantics and by mathematics (hand-worked example, closed forms, brute force,
+invariants). No function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "linr_oracle.cpp")
+_LIB = os.path.join(_HERE, "liblinr_oracle.so")
+_lib = None
+
+F32, F16, BF16, I8 = 0, 1, 2, 3
+
+CLAUSE_DTYPE = np.dtype([("mask", "<u8"), ("word", "u1"), ("reverse", "u1"), ("pad", "u1", 6)])
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain g++ (no intrinsics, no BLAS)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        L.oracle_widen.argtypes = [ctypes.c_int, ctypes.c_uint32]
+        L.oracle_widen.restype = ctypes.c_double
+        L.oracle_filter.argtypes = [P, ctypes.c_int, ctypes.c_int64, P, P, ctypes.c_int, P]
+        L.oracle_filter.restype = ctypes.c_int64
+        L.oracle_scores.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, P, P, P]
+        L.oracle_scores.restype = None
+        L.oracle_search.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, P,
+                                    P, ctypes.c_int, P, P, ctypes.c_int, ctypes.c_int,
+                                    P, P, ctypes.c_int, P, P, P]
+        L.oracle_search.restype = ctypes.c_int
+        L.oracle_merge.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P,
+                                   ctypes.c_int, P, P, P]
+        L.oracle_merge.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def clause_array(clauses_flat):
+    """list of (mask, word, reverse) -> structured array matching the 16-byte clause record."""
+    arr = np.zeros(len(clauses_flat), dtype=CLAUSE_DTYPE)
+    for i, (m, w, r) in enumerate(clauses_flat):
+        arr[i]["mask"] = m
+        arr[i]["word"] = w
+        arr[i]["reverse"] = r
+    return arr
+
+
+def csr(clauses):
+    flat, off = [], [0]
+    for cl in clauses:
+        flat.extend(cl)
+        off.append(len(flat))
+    return clause_array(flat), np.array(off, dtype=np.int32)
+
+
+def widen(dtype: int, bits: int) -> float:
+    return lib().oracle_widen(dtype, bits)
+
+
+def filter_mask(attrs, live, clauses_one):
+    attrs = np.ascontiguousarray(attrs, dtype=np.uint64)
+    n, W = attrs.shape
+    live = np.ascontiguousarray(live, dtype=np.uint8)
+    ca = clause_array(clauses_one)
+    out = np.zeros(n, dtype=np.uint8)
+    cnt = lib().oracle_filter(_p(attrs), W, n, _p(live), _p(ca), len(ca), _p(out))
+    return out.astype(bool), int(cnt)
+
+
+def scores(dtype, emb, q):
+    emb = np.ascontiguousarray(emb)
+    q = np.ascontiguousarray(q)
+    n, d = emb.shape
+    out = np.zeros(n, dtype=np.float64)
+    lib().oracle_scores(dtype, d, n, _p(emb), _p(q), _p(out))
+    return out
+
+
+def search(dtype, emb, attrs, live, queries, clauses, K, row0=0):
+    """Oracle top-K. emb [n][d] storage repr; attrs [n][W]; live [n]; queries [B][V][d] or [B][d].
+
+    Returns (ids [B][K] int64, scores [B][K] float64, pass [B] int64).
+    """
+    emb = np.ascontiguousarray(emb)
+    attrs = np.ascontiguousarray(attrs, dtype=np.uint64)
+    n, d = emb.shape if emb.ndim == 2 else (0, queries.shape[-1])
+    if n == 0:
+        emb = np.zeros((1, d), dtype=queries.dtype)
+        attrs = np.zeros((1, max(1, attrs.shape[1] if attrs.ndim == 2 else 1)), dtype=np.uint64)
+    W = attrs.shape[1]
+    live = np.ascontiguousarray(live, dtype=np.uint8) if n else np.zeros(1, np.uint8)
+    q = np.ascontiguousarray(queries)
+    if q.ndim == 2:
+        q = q[:, None, :]
+    B, V, _ = q.shape
+    ca, off = csr(clauses)
+    if len(ca) == 0:
+        ca = np.zeros(1, dtype=CLAUSE_DTYPE)
+    ids = np.zeros((B, K), dtype=np.int64)
+    sc = np.zeros((B, K), dtype=np.float64)
+    ps = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_search(dtype, d, n, row0, _p(emb), _p(attrs), W, _p(live), _p(q), B, V,
+                             _p(ca), _p(off), K, _p(ids), _p(sc), _p(ps))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return ids, sc, ps
+
+
+def merge(ids, scores_, pass_, K):
+    """Union of per-shard results [L][B][Kin] -> top-K [B][K]."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    scores_ = np.ascontiguousarray(scores_, dtype=np.float64)
+    pass_ = np.ascontiguousarray(pass_, dtype=np.int64)
+    L, B, Kin = ids.shape
+    oi = np.zeros((B, K), dtype=np.int64)
+    osc = np.zeros((B, K), dtype=np.float64)
+    op = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_merge(L, B, Kin, _p(ids), _p(scores_), _p(pass_), K, _p(oi), _p(osc), _p(op))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return oi, osc, op

@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the LiNR pre-filtered exhaustive top-K scan on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on): 10M items per GPU,
+d=128 bf16, one u64 attribute bitmask word per item, HIGH clause preset (geo Match 3/24 +
+company Reverse 1/16 = 11.7% pass, the paper's high-pass dataset analog),
+query batch B=1, K=1000. A step = one linr_search (fused filter+score+CTA top-K scan, then the
+merge kernel); for N>1 each rank holds its own 10M-row shard of a 10M*N-row index (weak scaling)
+and a step adds the all-gather of K packed keys (torch.distributed/NCCL) and the merge kernel.
+
+value = aggregate items scanned per second (B * index rows / step time, max over ranks);
+qps is reported next to it. e2e = the same metric through the host-buffer path
+(linr_search_host: query H2D + search + ids/scores/pass D2H + sync every step).
+
+--impl reference times the CPU oracle (oracle/, the reference arm of this tier) on a bounded
+sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filtered top-K QPS and items-scanned/s at 1/2/4/8 B200; % HBM roofline"
+N_ITEMS = 10_000_000
+DIM = 128
+K = 1000
+B = 1
+PRESET = "HIGH"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="linr", choices=["linr", "reference"])
+    ap.add_argument("--batch", type=int, default=B)
+    ap.add_argument("--preset", default=PRESET)
+    ap.add_argument("--items", type=int, default=N_ITEMS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(args, n_items):
+    return (f"c2: {n_items // 1_000_000}M items/GPU d={DIM} bf16, 64-bit attribute bitmask pre-filter "
+            f"({args.preset}), B={args.batch}, K={K}")
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, gpu_index: int):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per scan launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
+def oracle_sample(args, seconds_target=12.0, max_rows=2_000_000):
+    """Time the CPU oracle as it stands (single thread) on a bounded slice of the same workload."""
+    import numpy as np
+    import datagen as dg
+    import oracle
+    rows = min(max_rows, args.items)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, dg.BF16, dg.MODE_DENSE)
+    live = np.ones(rows, np.uint8)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, dg.BF16)
+    cls = dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset)
+    oracle.lib()
+    done_items, t_total, calls = 0, 0.0, 0
+    while t_total < seconds_target or calls == 0:
+        t0 = time.perf_counter()
+        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+        t_total += time.perf_counter() - t0
+        done_items += rows * args.batch
+        calls += 1
+        if calls >= 50:
+            break
+    ips = done_items / t_total
+    return {"items_per_s": ips, "qps_equiv": ips / args.items, "rows": rows, "calls": calls, "seconds": t_total}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import datagen as dg
+    import oracle
+    rows = min(1_000_000, args.items)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, dg.BF16, dg.MODE_DENSE)
+    live = np.ones(rows, np.uint8)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, dg.BF16)
+    cls = dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset)
+    oracle.lib()
+    for _ in range(args.warmup):
+        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+    dt = time.perf_counter() - t0
+    ips = rows * args.batch * args.steps / dt
+    sample = f"first {rows} rows of the {args.items}-row workload per step, B={args.batch}, single thread"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ips, "unit": "items/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "qps": ips / args.items,
+        "config": {"workload": workload_name(args, args.items), "n_items_per_gpu": args.items, "batch": args.batch,
+                   "K": K, "preset": args.preset, "parallelism": "host cores (oracle, 1 thread)"},
+        "cpu_baseline": {"value": ips, "unit": "items/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": ips, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen as dg
+    from paper_2407_13218_b200 import Index, ShardedIndex
+    from paper_2407_13218_b200.linr import Clauses
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_local = args.items
+    n_total = n_local * world
+
+    t_build = time.perf_counter()
+    if world > 1:
+        sidx = ShardedIndex(n_total, DIM, dg.BF16, 1, device=dev)
+        sidx.generate(dg.DATA_SEED, dg.MODE_DENSE)
+        ix = sidx.local
+    else:
+        sidx = None
+        ix = Index(n_local, DIM, dg.BF16, 1, device=dev)
+        ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, n_local)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n_total, args.batch, 1, DIM, dg.BF16)
+    qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16).contiguous()
+    qd = qh.to(dev)
+    qpin = qh.pin_memory()
+    cls = Clauses(dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+
+    ids = torch.empty((args.batch, K), dtype=torch.int64, device=dev)
+    sc = torch.empty((args.batch, K), dtype=torch.float32, device=dev)
+    ps = torch.empty(args.batch, dtype=torch.int64, device=dev)
+
+    def step():
+        if sidx is not None:
+            return sidx.search(qd, cls, K)
+        return ix.search(qd, cls, K, out=(ids, sc, ps))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    pass_count = int(step()[2][0].item())
+
+    # ---------------- device-timed region
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    ix.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = ix.profile_read()
+    ix.profile(False)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # ---------------- e2e through the host-buffer public API
+    if sidx is None:
+        hids = torch.empty((args.batch, K), dtype=torch.int64, pin_memory=True)
+        hsc = torch.empty((args.batch, K), dtype=torch.float32, pin_memory=True)
+        hps = torch.empty(args.batch, dtype=torch.int64, pin_memory=True)
+        for _ in range(3):
+            ix.search_host(qpin, cls, K, out=(hids, hsc, hps))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ix.search_host(qpin, cls, K, out=(hids, hsc, hps))
+        e2e_s = time.perf_counter() - t0
+    else:
+        for _ in range(3):
+            r = sidx.search(qpin.to(dev, non_blocking=True), cls, K)
+            r[0].cpu(), r[1].cpu(), r[2].cpu()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = sidx.search(qpin.to(dev, non_blocking=True), cls, K)
+            r[0].cpu(), r[1].cpu(), r[2].cpu()
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = args.batch * DIM * 2
+    d2h = args.batch * K * (8 + 4) + args.batch * 8
+
+    items_per_step = args.batch * n_total
+    value = items_per_step / (ms_step / 1e3)
+    e2e_value = items_per_step * args.steps / e2e_s
+
+    # roofline of the dominant kernel (the fused scan): algorithmic bytes per launch
+    # = per item 8 B attribute word + 1/8 B liveness bit, + per passing item the row (256 B)
+    rowbytes = DIM * 2
+    alg_bytes = n_local * (8 + 1 / 8) + pass_count * rowbytes if args.batch == 1 else None
+    scan_ms = prof["scan_ms"] / max(1, prof["searches"])
+    peak, peak_src = measured_peaks()
+    roof = None
+    if alg_bytes is not None and scan_ms > 0:
+        ach = alg_bytes / (scan_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": ncu_traffic(), "kernel": "scan_gemv_kernel<bf16,128,1>",
+                "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
+                "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+
+    launches_per_step = prof["launches"] / max(1, prof["searches"])
+    if world > 1:
+        launches_per_step += 1   # merge kernel after the all-gather
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            o = oracle_sample(args)
+            cpu = {"value": o["items_per_s"], "unit": "items/s", "cores": 1, "kind": "oracle",
+                   "sample": f"oracle (single thread, fp64) over the first {o['rows']} rows of the same workload, "
+                             f"B={args.batch}, {o['calls']} calls in {o['seconds']:.1f}s; qps_equiv="
+                             f"{o['qps_equiv']:.4g} for the {args.items}-row index"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (datagen recipe, generated on device)",
+            "qps": args.batch / (ms_step / 1e3),
+            "config": {"workload": workload_name(args, n_local), "n_items_per_gpu": n_local, "n_items_total": n_total,
+                       "batch": args.batch, "K": K, "dim": DIM, "preset": args.preset, "pass_count": pass_count,
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (index 2.56 GB/GPU > 126 MB L2; no flush needed)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "items/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s / args.steps * 1e3},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clk,
+            "build_s": round(t_build, 2),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

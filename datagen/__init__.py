@@ -87,9 +87,12 @@ def h2(seed: int, stream: int, a, b):
 # ---------------------------------------------------------------- rounding helpers
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even fp32 -> bf16, returned as uint16 bit patterns (finite inputs)."""
-    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    u = u + U64(0x7FFF) + ((u >> U64(16)) & U64(1))
-    return (u >> U64(16)).astype(np.uint16)
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = (u >> np.uint32(16)) & np.uint32(1)
+    r += np.uint32(0x7FFF)
+    r += u                      # finite inputs: no uint32 overflow (max 0xFF7FFFFF + 0x8000)
+    r >>= np.uint32(16)
+    return r.astype(np.uint16)
 
 
 def f32_to_f16_bits(x: np.ndarray) -> np.ndarray:
@@ -118,34 +121,52 @@ def _store(x32: np.ndarray, dtype: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- items
+_CENTER_CACHE: dict = {}
+
+
+def _center_table(seed: int, d: int, kind: str) -> np.ndarray:
+    """Per-cluster centers [N_CLUSTERS][d]: int16 codes in [-64,63] ('i8') or exact fp32 in [-0.5,0.5) ('f')."""
+    key = (seed, d, kind)
+    t = _CENTER_CACHE.get(key)
+    if t is None:
+        cl = np.arange(N_CLUSTERS, dtype=U64)
+        if kind == "i8":
+            nb = (d + 7) // 8
+            h = h2(seed, S_CENTER, cl[:, None], np.arange(nb, dtype=U64)[None, :])      # [C, nb]
+            t = (h.view(np.uint8).reshape(N_CLUSTERS, nb * 8)[:, :d] & np.uint8(0x7F)).astype(np.int16) - 64
+        else:
+            nc = (d + 1) // 2
+            h = h2(seed, S_CENTER, cl[:, None], np.arange(nc, dtype=U64)[None, :])      # [C, nc]
+            c24 = h.view(np.uint32).reshape(N_CLUSTERS, nc * 2)[:, :d] & np.uint32(0xFFFFFF)
+            t = c24.astype(np.float32) * np.float32(2.0 ** -24) - np.float32(0.5)
+        _CENTER_CACHE[key] = t
+    return t
+
+
+def _clusters(seed: int, rows: np.ndarray) -> np.ndarray:
+    return (h1(seed, S_CLUSTER, rows) & U64(N_CLUSTERS - 1)).astype(np.int64)
+
+
 def _int8_values(seed: int, rows: np.ndarray, d: int) -> np.ndarray:
-    """int8 codes x = center[cluster(row)] + noise(row), center in [-64,63], noise in [-32,31]."""
+    """int8 codes x = center[cluster(row)] + noise(row), center in [-64,63], noise in [-32,31].
+    Byte k of a 64-bit hash feeds element 8*blk + k (little-endian byte order)."""
     rows = np.asarray(rows, dtype=U64)
-    cl = h1(seed, S_CLUSTER, rows) & U64(N_CLUSTERS - 1)                     # [n]
+    cen = _center_table(seed, d, "i8")[_clusters(seed, rows)]                    # [n, d] int16
     nb = (d + 7) // 8
-    blk = np.arange(nb, dtype=U64)
-    cen_h = h2(seed, S_CENTER, cl[:, None], blk[None, :])                    # [n, nb]
-    noi_h = h2(seed, S_NOISE, rows[:, None], blk[None, :])                   # [n, nb]
-    sh = (np.arange(8, dtype=U64) * U64(8))
-    cen = ((cen_h[:, :, None] >> sh) & U64(0x7F)).astype(np.int16) - 64      # [n, nb, 8]
-    noi = ((noi_h[:, :, None] >> sh) & U64(0x3F)).astype(np.int16) - 32
-    v = (cen + noi).reshape(len(rows), nb * 8)[:, :d]
-    return np.clip(v, -127, 127).astype(np.int8)
+    noi_h = h2(seed, S_NOISE, rows[:, None], np.arange(nb, dtype=U64)[None, :])  # [n, nb]
+    noi = (noi_h.view(np.uint8).reshape(len(rows), nb * 8)[:, :d] & np.uint8(0x3F)).astype(np.int16) - 32
+    return np.clip(cen + noi, -127, 127).astype(np.int8)
 
 
 def _dense_values(seed: int, rows: np.ndarray, d: int) -> np.ndarray:
-    """fp32 values fl32(c + n): c = u24*2^-24 - 0.5 per (cluster, j), n = u16*2^-17 - 0.25 per (row, j)."""
+    """fp32 values fl32(c + n): c = u24*2^-24 - 0.5 per (cluster, j) from the low 24 bits of 32-bit
+    half (j % 2) of h2(center, cluster, j//2); n = u16*2^-17 - 0.25 per (row, j) from 16-bit
+    quarter (j % 4) of h2(noise, row, j//4)."""
     rows = np.asarray(rows, dtype=U64)
-    cl = h1(seed, S_CLUSTER, rows) & U64(N_CLUSTERS - 1)
-    nc = (d + 1) // 2
-    cen_h = h2(seed, S_CENTER, cl[:, None], np.arange(nc, dtype=U64)[None, :])
-    sh2 = np.array([0, 32], dtype=U64)
-    c24 = ((cen_h[:, :, None] >> sh2) & U64(0xFFFFFF)).reshape(len(rows), nc * 2)[:, :d]
-    c = c24.astype(np.float32) * np.float32(2.0 ** -24) - np.float32(0.5)
+    c = _center_table(seed, d, "f")[_clusters(seed, rows)]                         # [n, d] fp32
     nn = (d + 3) // 4
-    noi_h = h2(seed, S_NOISE, rows[:, None], np.arange(nn, dtype=U64)[None, :])
-    sh4 = np.array([0, 16, 32, 48], dtype=U64)
-    n16 = ((noi_h[:, :, None] >> sh4) & U64(0xFFFF)).reshape(len(rows), nn * 4)[:, :d]
+    noi_h = h2(seed, S_NOISE, rows[:, None], np.arange(nn, dtype=U64)[None, :])   # [n, nn]
+    n16 = noi_h.view(np.uint16).reshape(len(rows), nn * 4)[:, :d]
     n = n16.astype(np.float32) * np.float32(2.0 ** -17) - np.float32(0.25)
     return (c + n).astype(np.float32)
 
@@ -179,9 +200,31 @@ def item_attrs(seed: int, rows, W: int) -> np.ndarray:
     return out
 
 
-def gen_items(seed: int, row_begin: int, n: int, d: int, dtype: int, mode: int = MODE_DENSE, W: int = 1):
-    rows = np.arange(row_begin, row_begin + n, dtype=np.int64)
-    return item_values(seed, rows, d, dtype, mode), item_attrs(seed, rows, W)
+def gen_items(seed: int, row_begin: int, n: int, d: int, dtype: int, mode: int = MODE_DENSE, W: int = 1,
+              threads: int = 0):
+    """Rows [row_begin, row_begin+n): (values [n][d] storage repr, attrs [n][W] uint64).
+    Large requests are split into row chunks on a thread pool (numpy releases the GIL); the
+    result is identical because every value is a function of its (row, col) counter."""
+    chunk = 1 << 18
+    if n <= chunk:
+        rows = np.arange(row_begin, row_begin + n, dtype=np.int64)
+        return item_values(seed, rows, d, dtype, mode), item_attrs(seed, rows, W)
+    import concurrent.futures as cf
+    import os
+    vdt = {F32: np.float32, F16: np.uint16, BF16: np.uint16, I8: np.int8}[dtype]
+    vals = np.empty((n, d), dtype=vdt)
+    attrs = np.empty((n, W), dtype=U64)
+    _center_table(seed, d, "i8" if (dtype == I8 or mode == MODE_GRID) else "f")
+
+    def work(a):
+        b = min(n, a + chunk)
+        rows = np.arange(row_begin + a, row_begin + b, dtype=np.int64)
+        vals[a:b] = item_values(seed, rows, d, dtype, mode)
+        attrs[a:b] = item_attrs(seed, rows, W)
+
+    with cf.ThreadPoolExecutor(threads or min(32, os.cpu_count() or 4)) as ex:
+        list(ex.map(work, range(0, n, chunk)))
+    return vals, attrs
 
 
 # ---------------------------------------------------------------- queries
@@ -200,8 +243,7 @@ def gen_queries(qseed: int, dseed: int, n_items: int, B: int, V: int, d: int, dt
         base = _int8_values(dseed, src, d).astype(np.int16)
         nb = (d + 7) // 8
         hq = h2(qseed, S_QNOISE, ctr[:, None], np.arange(nb, dtype=U64)[None, :])
-        sh = np.arange(8, dtype=U64) * U64(8)
-        nz = ((hq[:, :, None] >> sh) & U64(0xF)).astype(np.int16).reshape(len(src), nb * 8)[:, :d] - 8
+        nz = (hq.view(np.uint8).reshape(len(src), nb * 8)[:, :d] & np.uint8(0xF)).astype(np.int16) - 8
         q8 = np.clip(base + nz, -127, 127).astype(np.int8)
         if dtype == I8:
             out = q8
@@ -211,8 +253,7 @@ def gen_queries(qseed: int, dseed: int, n_items: int, B: int, V: int, d: int, dt
         base = bits_to_f32(item_values(dseed, src, d, dtype, mode), dtype)
         nn = (d + 3) // 4
         hq = h2(qseed, S_QNOISE, ctr[:, None], np.arange(nn, dtype=U64)[None, :])
-        sh4 = np.array([0, 16, 32, 48], dtype=U64)
-        n16 = ((hq[:, :, None] >> sh4) & U64(0xFFFF)).reshape(len(src), nn * 4)[:, :d]
+        n16 = hq.view(np.uint16).reshape(len(src), nn * 4)[:, :d]
         nz = n16.astype(np.float32) * np.float32(2.0 ** -18) - np.float32(0.125)
         out = _store((base + nz).astype(np.float32), dtype)
     return out.reshape(B, V, d)

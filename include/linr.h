@@ -1,0 +1,202 @@
+/*
+ * linr.h — C ABI of the B200-native LiNR pre-filtered exhaustive top-K scan.
+ *
+ * The operation (arXiv 2407.13218, §3.1 "Exhaustive Search with Attribute-Based
+ * Matching"): for each query, evaluate its boolean attribute clauses against every
+ * item's attribute bitmask ("Feasible items should satisfy all clauses, requiring at least one of
+ * the attribute in each clauses is matched. Reverse clauses are also supported"), score
+ * every surviving item by dot product with the query embedding ("KNN uses dot-product
+ * similarity"), and return the best K (score, item-id) pairs ("Top-1 selection",
+ * top-2k in §5.3). Filtered items are excluded, never scored as zero (DESIGN.md reading
+ * R1). Live updates overwrite rows in place in pre-allocated storage under a high-water mark
+ * (§4.3 "Model Live Update").
+ *
+ * Conventions shared by every entry point
+ *  - Every call returns a linr_status (0 = OK). No C++ exception crosses the ABI. On failure
+ *    linr_last_error() returns a thread-local message. Validation happens before anything is
+ *    enqueued; asynchronous CUDA errors are sticky and surface as LINR_ECUDA on a later call.
+ *  - "_dev" pointers are CUDA device pointers on the index's device; "_host" pointers are host
+ *    memory (pinned or pageable). All data buffers are caller-owned (PyTorch allocates them);
+ *    the library never frees them and they must outlive every call that uses them.
+ *  - `stream` is a cudaStream_t passed as void*. All device work is enqueued on it; calls
+ *    return before the work finishes, except linr_search_host and linr_index_stats, which
+ *    synchronise `stream`. A search observes exactly the updates enqueued before it on the same
+ *    stream (snapshot consistency by stream order; reading R16). Unordered concurrent use of one
+ *    index from two streams is undefined.
+ *  - Item ids are global row ids: local row r of a shard has id global_row0 + r (int64 in the
+ *    ABI, < 2^32-1 internally). Results are ordered by score descending, then id ascending
+ *    (reading R5); slots past min(K, pass_count) hold id -1 and score -inf (reading R6).
+ *  - Scores are returned as fp32: float dtypes accumulate in fp32 (reading R8); int8 scores are
+ *    exact integer dot products, exactly representable in fp32 for dim <= 1024 (reading R10).
+ */
+#ifndef LINR_H_
+#define LINR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct linr_index linr_index; /* opaque: library-owned metadata only */
+
+typedef enum {
+  LINR_OK = 0,
+  LINR_EINVAL = -1,       /* bad argument (null pointer, shape, clause, dtype …)        */
+  LINR_ERANGE = -2,       /* row range outside [global_row0, global_row0 + capacity)     */
+  LINR_ENOMEM = -3,       /* workspace too small / host allocation failed                */
+  LINR_ECUDA = -4,        /* CUDA launch / runtime error (sticky asynchronous errors too) */
+  LINR_EUNSUPPORTED = -6  /* valid but not built (e.g. a dim with no compiled kernel)     */
+} linr_status;
+
+typedef enum { LINR_F32 = 0, LINR_F16 = 1, LINR_BF16 = 2, LINR_I8 = 3 } linr_dtype;
+
+/* One clause of a query (16 bytes, host memory).
+ * passes(item) = ((attrs[item][word] & mask) != 0) XOR reverse
+ * mask: the clause's attribute set as bits of attribute word `word` (reading R2: a clause lists
+ *       attribute values; OR within the clause = any bit overlaps). mask == 0 is rejected
+ *       (EINVAL; reading R3 — omit the clause to disable it).
+ * word: attribute word index, < attr_words.  reverse: 0 = Match, 1 = Reverse. */
+typedef struct {
+  uint64_t mask;
+  uint8_t word;
+  uint8_t reverse;
+  uint8_t pad[6];
+} linr_clause;
+
+#define LINR_MAX_K 2048          /* K range 1..2048 (paper uses K=2000; reading R14) */
+#define LINR_MAX_V 8             /* query vectors per user (multi-embedding, reading R12)     */
+#define LINR_MAX_CLAUSES 16      /* clauses per query                                         */
+#define LINR_MAX_ATTR_WORDS 4    /* u64 attribute words per item                              */
+
+typedef struct {
+  int64_t capacity_rows; /* rows pre-allocated on this shard ("pre-allocating larger tensors") */
+  int64_t global_row0;   /* global id of local row 0 (row sharding)                                 */
+  int32_t dim;           /* d: power of two in [16, 1024]                                           */
+  int32_t dtype;         /* linr_dtype of items AND queries                                         */
+  int32_t attr_words;    /* W in [1, 4]                                                             */
+  int32_t device;        /* CUDA device ordinal the storage lives on                                */
+  void* emb_storage;     /* device, linr_storage_bytes(desc, 0) bytes, caller-owned                 */
+  void* attr_storage;    /* device, linr_storage_bytes(desc, 1) bytes                               */
+  void* live_storage;    /* device, linr_storage_bytes(desc, 2) bytes; MUST be zero-filled at create */
+} linr_index_desc;
+
+/* Bytes the caller must allocate for storage `which` (0 emb, 1 attrs, 2 live bitmap + device
+ * header incl. the high-water mark). Capacity is padded internally to a multiple of 256 rows.
+ * Returns 0 for an invalid desc/which. Layout is private to the library. */
+size_t linr_storage_bytes(const linr_index_desc* desc, int which);
+
+/* Validate desc and create a handle over the caller's storage. live_storage must be zeroed
+ * (no row live, high-water mark 0: "empty index; high_water_mark = 0"). */
+int linr_index_create(const linr_index_desc* desc, linr_index** out);
+void linr_index_destroy(linr_index* index);
+
+/* Bulk load rows [row0, row0+n) (global ids) from device buffers:
+ *   emb_dev   [n][dim] row-major in the index dtype;  attrs_dev [n][attr_words] u64 row-major.
+ * Marks the rows live and raises the high-water mark ("using a high-water mark").
+ * ERANGE if the range leaves the shard. n == 0 is a no-op. */
+int linr_index_load(linr_index* index, int64_t row0, int64_t n, const void* emb_dev,
+                    const uint64_t* attrs_dev, void* stream);
+
+/* Live upsert (§4.3, "expose Upsert and Delete APIs"): overwrite rows
+ * rows_dev[0..n) (global ids, device int64) in place with emb_dev [n][dim], attrs_dev [n][W];
+ * mark them live; raise the high-water mark. Ids outside this shard are skipped on the device
+ * and counted (linr_index_stats). If an id repeats within one call, which copy wins is
+ * unspecified. A search on the same stream sees each row wholly old or wholly new. */
+int linr_index_update_rows(linr_index* index, const int64_t* rows_dev, int64_t n,
+                           const void* emb_dev, const uint64_t* attrs_dev, void* stream);
+
+/* Live delete: clear the liveness bit of rows_dev[0..n) (tombstone; reading R7). The
+ * high-water mark never decreases. Out-of-shard ids are skipped and counted. */
+int linr_index_delete_rows(linr_index* index, const int64_t* rows_dev, int64_t n, void* stream);
+
+/* Synchronising read of the device header: high-water mark (local rows), the number of
+ * out-of-shard ids skipped by update/delete so far, and the number of scan-buffer overflows (an
+ * internal invariant that must stay 0; tests assert it). Any output may be NULL. */
+int linr_index_stats(linr_index* index, int64_t* hwm_host, int64_t* skipped_host,
+                     int64_t* scan_overflow_host, void* stream);
+
+/* Workspace bytes needed by linr_search / linr_search_keys for (B, V, K). 0 if invalid. */
+size_t linr_search_workspace_bytes(const linr_index* index, int32_t B, int32_t V, int32_t K);
+
+/* The hot path: filtered exhaustive top-K over this shard.
+ *   queries_dev  [B][V][dim] in the index dtype (V <= LINR_MAX_V query vectors per user; score =
+ *                max over the user's V dot products, reading R12)
+ *   clauses_host  all clauses, CSR by clause_off_host[B+1] (host int32, non-decreasing,
+ *                 clause_off_host[0] == 0, at most LINR_MAX_CLAUSES per query)
+ *   ws_dev        device workspace of >= linr_search_workspace_bytes(index, B, V, K) bytes
+ *   out_ids_dev [B][K] int64, out_scores_dev [B][K] fp32, out_pass_dev [B] int64 (may be NULL:
+ *                 number of live items passing each query's clauses)
+ * EINVAL on: null pointers, B < 1, V < 1 or > LINR_MAX_V, K < 1 or > LINR_MAX_K, bad offsets,
+ * clause word >= W, clause mask == 0, too many clauses. */
+int linr_search(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
+                const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
+                void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, float* out_scores_dev,
+                int64_t* out_pass_dev, void* stream);
+
+/* Shard-local variant for row-sharded indexes: same inputs as linr_search, output is this
+ * shard's top-K as packed keys out_keys_dev [B][K] u64 (sorted descending, 0-padded) plus
+ * out_pass_dev [B] int64. key = (ordered_u32(score) << 32) | (0xFFFFFFFF - global_id), where
+ * ordered_u32 maps fp32 order to unsigned order (-0.0 as +0.0); larger key = better result. The
+ * keys of all shards are exchanged (all-gather over torch.distributed/NCCL) and merged by
+ * linr_merge_keys. */
+int linr_search_keys(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
+                     const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
+                     void* ws_dev, size_t ws_bytes, uint64_t* out_keys_dev, int64_t* out_pass_dev,
+                     void* stream);
+
+/* Workspace for linr_merge_keys. */
+size_t linr_merge_workspace_bytes(int32_t L, int32_t B, int32_t K);
+
+/* Merge L shard results (BASELINE.json north_star: "allgather of K (score, item-id) pairs ...
+ * feeds a final merge"; reading R13: union then top-K under the same total order):
+ *   keys_dev [L][B][K] u64 (each list sorted descending, 0-padded), pass_dev [L][B] int64
+ * -> out_ids_dev [B][K] int64, out_scores_dev [B][K] fp32, out_pass_dev [B] (sum; may be NULL). */
+int linr_merge_keys(const uint64_t* keys_dev, const int64_t* pass_dev, int32_t L, int32_t B,
+                    int32_t K, void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev,
+                    float* out_scores_dev, int64_t* out_pass_dev, void* stream);
+
+/* End-to-end convenience call with HOST buffers (the e2e path the benchmark times): copies
+ * queries_host [B][V][dim] to the device, runs linr_search, copies ids/scores/pass back to
+ * out_ids_host [B][K], out_scores_host [B][K], out_pass_host [B] (may be NULL) and synchronises
+ * `stream`. ws_dev must hold linr_search_workspace_bytes(...) + linr_search_host_extra_bytes(...). */
+size_t linr_search_host_extra_bytes(const linr_index* index, int32_t B, int32_t V, int32_t K);
+int linr_search_host(linr_index* index, const void* queries_host, int32_t B, int32_t V,
+                     const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
+                     void* ws_dev, size_t ws_bytes, int64_t* out_ids_host, float* out_scores_host,
+                     int64_t* out_pass_host, void* stream);
+
+/* Device-side synthetic data generator (benchmark plumbing, not part of the method): fills local
+ * rows [row_begin, row_begin+n) of the index with the counter-based recipe of DESIGN.md
+ * "Input recipe" (identical bytes to datagen/ in Python), marks them live and raises the
+ * high-water mark. Lets 1B-row shards be built in place. mode: 0 integer grid, 1 dense. */
+int linr_index_generate(linr_index* index, uint64_t seed, int32_t mode, int64_t row_begin,
+                        int64_t n, void* stream);
+
+/* Generate rows [row_begin, row_begin+n) into plain device buffers (no index): emb_dev
+ * [n][dim] dtype, attrs_dev [n][W] (either may be NULL). Used by the generator cross-check. */
+int linr_generate_rows(int32_t dtype, int32_t dim, int32_t attr_words, uint64_t seed, int32_t mode,
+                       int64_t row_begin, int64_t n, void* emb_dev, uint64_t* attrs_dev,
+                       void* stream);
+
+/* Stage timing for benchmarks (measured on the search stream with CUDA events, no extra sync
+ * on the hot path): while enabled, every linr_search / linr_search_keys / linr_search_host on
+ * this index records events around its scan launches and its merge launch.
+ * linr_index_profile_read synchronises the recorded events, returns the summed scan and merge
+ * milliseconds, the number of searches and the number of this library's kernel launches since
+ * the last read, and resets the counters. */
+int linr_index_profile(linr_index* index, int enable);
+int linr_index_profile_read(linr_index* index, double* scan_ms, double* merge_ms, int64_t* searches,
+                            int64_t* kernel_launches);
+
+/* Thread-local message for the last non-OK return on this thread ("" if none). */
+const char* linr_last_error(void);
+
+/* ABI version (incremented on any signature change). */
+int linr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINR_H_ */

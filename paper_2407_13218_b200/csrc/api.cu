@@ -1,0 +1,559 @@
+// Host side of the C ABI declared in include/linr.h: validation, storage layout, launch planning.
+// Every step of the search runs in this library's kernels (scan_gemv.cuh, merge.cu); PyTorch only
+// supplies the device buffers and the stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace linr {
+cudaError_t launch_scan_gemv_f32(int, int, const ScanParams&, int, size_t, cudaStream_t);
+cudaError_t launch_scan_gemv_f16(int, int, const ScanParams&, int, size_t, cudaStream_t);
+cudaError_t launch_scan_gemv_bf16(int, int, const ScanParams&, int, size_t, cudaStream_t);
+cudaError_t launch_scan_gemv_i8(int, int, const ScanParams&, int, size_t, cudaStream_t);
+ScanCfg scan_cfg_f32(int, int);
+ScanCfg scan_cfg_f16(int, int);
+ScanCfg scan_cfg_bf16(int, int);
+ScanCfg scan_cfg_i8(int, int);
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+static int esize(int dt) { return dt == LINR_F32 ? 4 : (dt == LINR_I8 ? 1 : 2); }
+static bool dim_ok(int d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 512 || d == 1024; }
+static int64_t pad_rows(int64_t cap) { return (cap + kTileItems - 1) / kTileItems * kTileItems; }
+
+cudaError_t launch_scan_gemv(int dtype, int dim, int nqv, const ScanParams& p, int grid, size_t smem,
+                             cudaStream_t st) {
+  switch (dtype) {
+    case LINR_F32: return launch_scan_gemv_f32(dim, nqv, p, grid, smem, st);
+    case LINR_F16: return launch_scan_gemv_f16(dim, nqv, p, grid, smem, st);
+    case LINR_BF16: return launch_scan_gemv_bf16(dim, nqv, p, grid, smem, st);
+    case LINR_I8: return launch_scan_gemv_i8(dim, nqv, p, grid, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+ScanCfg scan_gemv_cfg(int dtype, int dim, int nqv) {
+  switch (dtype) {
+    case LINR_F32: return scan_cfg_f32(dim, nqv);
+    case LINR_F16: return scan_cfg_f16(dim, nqv);
+    case LINR_BF16: return scan_cfg_bf16(dim, nqv);
+    case LINR_I8: return scan_cfg_i8(dim, nqv);
+  }
+  return ScanCfg{0, 0};
+}
+// query registers per lane = nqv * (chunks per lane) * (fp32 values or packed words per chunk)
+bool scan_gemv_supported(int dtype, int dim, int nqv) {
+  if (!dim_ok(dim)) return false;
+  const int ch = dim * esize(dtype) / 16;
+  const int lpr = ch < 32 ? ch : 32;
+  const int cpl = ch / lpr;
+  const int per_chunk = dtype == LINR_I8 ? 4 : 16 / esize(dtype);
+  return nqv * cpl * per_chunk <= 64;
+}
+
+}  // namespace linr
+
+using namespace linr;
+
+struct ProfEvents {
+  cudaEvent_t e0, e1, e2;   // before scan, after scan (= before merge), after merge
+};
+
+struct linr_index {
+  linr_index_desc d;
+  bool prof = false;
+  std::vector<ProfEvents> prof_used, prof_free;
+  int64_t prof_launches = 0;
+  int64_t cap_pad;
+  int rowbytes;
+  int num_sms;
+  size_t smem_optin;
+  void* emb;
+  uint64_t* attr;
+  uint32_t* live;
+  DevHeader* hdr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1, want;
+  explicit DeviceGuard(int dev) : want(dev) {
+    cudaGetDevice(&prev);
+    if (prev != want) cudaSetDevice(want);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return LINR_ECUDA;
+}
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ----------------------------------------------------------------- search planning
+struct Plan {
+  int nu_g = 0;       // users per scan launch
+  int groups = 0;
+  int nqv = 0;
+  int nt = 0;
+  int C = 0, bufcap = 0;
+  size_t smem = 0;
+  int grid = 0;
+};
+
+constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) rounded (checked in scan_gemv.cuh users)
+
+bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why) {
+  const int dt = ix->d.dtype, dim = ix->d.dim;
+  const int p2k = next_pow2(K);
+  int nu = std::max(1, std::min(B, std::min(kMaxUsers, 8 / V)));
+  for (; nu >= 1; --nu) {
+    const int nqv = next_pow2(nu * V);
+    if (nqv > 8 || !scan_gemv_supported(dt, dim, nqv)) continue;
+    const ScanCfg cfg = scan_gemv_cfg(dt, dim, nqv);
+    if (cfg.nt == 0) continue;
+    const int head = (cfg.nt / 32) * cfg.rows_per_iter;
+    for (int C : {std::max(2 * p2k, 1024), p2k + 512}) {
+      if (C <= K) continue;
+      const int bufcap = std::max(C + head, p2k);
+      const size_t smem = kScanCtlBytes + (size_t)nu * bufcap * 8 + (size_t)(cfg.nt / 32) * kTileItems * 2;
+      if (smem <= ix->smem_optin) {
+        pl->nu_g = nu;
+        pl->groups = (B + nu - 1) / nu;
+        pl->nqv = nqv;
+        pl->nt = cfg.nt;
+        pl->C = C;
+        pl->bufcap = bufcap;
+        pl->smem = smem;
+        pl->grid = ix->num_sms;
+        return true;
+      }
+    }
+  }
+  *why = "no GEMV scan configuration fits (dtype " + std::to_string(dt) + ", dim " + std::to_string(dim) +
+         ", V " + std::to_string(V) + ", K " + std::to_string(K) + ")";
+  return false;
+}
+
+struct WsLayout {
+  size_t lists = 0, pass = 0, end = 0;
+};
+WsLayout ws_layout(const Plan& pl, int B, int K) {
+  WsLayout w;
+  w.lists = 0;
+  w.pass = align256((size_t)B * pl.grid * K * 8);
+  w.end = w.pass + align256((size_t)B * pl.grid * 8);
+  return w;
+}
+
+int validate_query(const linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off,
+                   int K, std::string* why) {
+  if (!ix) { *why = "null index"; return LINR_EINVAL; }
+  if (!q) { *why = "null queries"; return LINR_EINVAL; }
+  if (B < 1) { *why = "B must be >= 1"; return LINR_EINVAL; }
+  if (V < 1 || V > 8) { *why = "V must be in [1, 8]"; return LINR_EINVAL; }
+  if (K < 1 || K > LINR_MAX_K) { *why = "K must be in [1, 2048]"; return LINR_EINVAL; }
+  if (!off) { *why = "null clause offsets"; return LINR_EINVAL; }
+  if (off[0] != 0) { *why = "clause_off[0] must be 0"; return LINR_EINVAL; }
+  for (int b = 0; b < B; ++b) {
+    const int n = off[b + 1] - off[b];
+    if (n < 0) { *why = "clause offsets must be non-decreasing"; return LINR_EINVAL; }
+    if (n > LINR_MAX_CLAUSES) { *why = "more than 16 clauses in one query"; return LINR_EINVAL; }
+    if (n > 0 && !cl) { *why = "null clauses"; return LINR_EINVAL; }
+    for (int c = off[b]; c < off[b + 1]; ++c) {
+      if (cl[c].mask == 0) { *why = "empty clause mask (omit the clause instead)"; return LINR_EINVAL; }
+      if (cl[c].word >= ix->d.attr_words) { *why = "clause word >= attr_words"; return LINR_EINVAL; }
+      if (cl[c].reverse > 1) { *why = "clause reverse must be 0 or 1"; return LINR_EINVAL; }
+    }
+  }
+  return LINR_OK;
+}
+
+// scan (+ per-CTA lists) then merge into either ids/scores (mode 0) or keys (mode 1)
+int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
+                void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
+                int64_t* out_pass, cudaStream_t st) {
+  std::string why;
+  int rc = validate_query(ix, q, B, V, cl, off, K, &why);
+  if (rc != LINR_OK) return fail(rc, why);
+  if (mode == 0 && (!out_ids || !out_scores)) return fail(LINR_EINVAL, "null outputs");
+  if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
+  Plan pl;
+  if (!make_plan(ix, B, V, K, &pl, &why)) return fail(LINR_EUNSUPPORTED, why);
+  const WsLayout wl = ws_layout(pl, B, K);
+  if (!ws || ws_bytes < wl.end) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+
+  uint64_t* lists = (uint64_t*)((char*)ws + wl.lists);
+  int64_t* pass = (int64_t*)((char*)ws + wl.pass);
+  ProfEvents pe{};
+  if (ix->prof) {
+    if (!ix->prof_free.empty()) {
+      pe = ix->prof_free.back();
+      ix->prof_free.pop_back();
+    } else {
+      cudaEventCreate(&pe.e0);
+      cudaEventCreate(&pe.e1);
+      cudaEventCreate(&pe.e2);
+    }
+    cudaEventRecord(pe.e0, st);
+  }
+  for (int g = 0; g < pl.groups; ++g) {
+    const int u0 = g * pl.nu_g;
+    const int nu = std::min(pl.nu_g, B - u0);
+    ScanParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.emb = ix->emb;
+    p.attr = ix->attr;
+    p.live = ix->live;
+    p.hdr = ix->hdr;
+    p.cap_pad = ix->cap_pad;
+    p.row0 = (uint32_t)ix->d.global_row0;
+    p.nu = nu;
+    p.V = V;
+    p.K = K;
+    p.C = pl.C;
+    p.bufcap = pl.bufcap;
+    p.q = (const char*)q + (size_t)u0 * V * ix->rowbytes;
+    p.out_keys = lists + (size_t)u0 * pl.grid * K;
+    p.out_pass = pass + (size_t)u0 * pl.grid;
+    uint32_t wmask = 0;
+    for (int u = 0; u < nu; ++u) {
+      const int b = u0 + u;
+      p.ncl[u] = off[b + 1] - off[b];
+      for (int c = 0; c < p.ncl[u]; ++c) {
+        const linr_clause& k = cl[off[b] + c];
+        p.cl[u][c].mask = k.mask;
+        p.cl[u][c].word = k.word;
+        p.cl[u][c].rev = k.reverse;
+        wmask |= 1u << k.word;
+      }
+    }
+    p.wmask = wmask;
+    e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, p, pl.grid, pl.smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+  }
+  if (ix->prof) cudaEventRecord(pe.e1, st);
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.keys = lists;
+  mp.stride_l = K;
+  mp.stride_u = (int64_t)pl.grid * K;
+  mp.pass = pass;
+  mp.pstride_l = 1;
+  mp.pstride_u = pl.grid;
+  mp.L = pl.grid;
+  mp.K = K;
+  mp.m = merge_sample_size(pl.grid, K);
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_keys = out_keys;
+  mp.out_pass = out_pass;
+  mp.mode = mode;
+  e = launch_merge(mp, B, st);
+  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  if (ix->prof) {
+    cudaEventRecord(pe.e2, st);
+    ix->prof_used.push_back(pe);
+    ix->prof_launches += pl.groups + 1;
+  }
+  return LINR_OK;
+}
+
+bool desc_ok(const linr_index_desc* d, std::string* why) {
+  if (!d) { *why = "null desc"; return false; }
+  if (d->capacity_rows < 1) { *why = "capacity_rows must be >= 1"; return false; }
+  if (d->global_row0 < 0 || d->global_row0 + d->capacity_rows > 0xFFFFFFFFll) {
+    *why = "global ids must be < 2^32-1";
+    return false;
+  }
+  if (d->dtype < LINR_F32 || d->dtype > LINR_I8) { *why = "bad dtype"; return false; }
+  if (d->dim < 16 || d->dim % 16) { *why = "dim must be a positive multiple of 16"; return false; }
+  if (d->attr_words < 1 || d->attr_words > LINR_MAX_ATTR_WORDS) { *why = "attr_words must be in [1,4]"; return false; }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int linr_version(void) { return 1; }
+const char* linr_last_error(void) { return g_err.c_str(); }
+
+size_t linr_storage_bytes(const linr_index_desc* d, int which) {
+  std::string why;
+  if (!desc_ok(d, &why)) return 0;
+  const int64_t cp = pad_rows(d->capacity_rows);
+  switch (which) {
+    case 0: return (size_t)cp * d->dim * esize(d->dtype);
+    case 1: return (size_t)cp * d->attr_words * 8;
+    case 2: return kHdrBytes + (size_t)cp / 32 * 4;
+  }
+  return 0;
+}
+
+int linr_index_create(const linr_index_desc* d, linr_index** out) {
+  std::string why;
+  if (!out) return fail(LINR_EINVAL, "null out");
+  *out = nullptr;
+  if (!desc_ok(d, &why)) return fail(LINR_EINVAL, why);
+  if (!dim_ok(d->dim)) return fail(LINR_EUNSUPPORTED, "dim must be a power of two in [16, 1024]");
+  if (!d->emb_storage || !d->attr_storage || !d->live_storage) return fail(LINR_EINVAL, "null storage");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (d->device < 0 || d->device >= ndev) return fail(LINR_EINVAL, "bad device");
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device);
+  linr_index* ix = new (std::nothrow) linr_index;
+  if (!ix) return fail(LINR_ENOMEM, "host allocation");
+  ix->d = *d;
+  ix->cap_pad = pad_rows(d->capacity_rows);
+  ix->rowbytes = d->dim * esize(d->dtype);
+  ix->num_sms = sms;
+  ix->smem_optin = (size_t)optin;
+  ix->emb = d->emb_storage;
+  ix->attr = (uint64_t*)d->attr_storage;
+  ix->hdr = (DevHeader*)d->live_storage;
+  ix->live = (uint32_t*)((char*)d->live_storage + kHdrBytes);
+  *out = ix;
+  return LINR_OK;
+}
+
+void linr_index_destroy(linr_index* ix) {
+  if (!ix) return;
+  for (auto* v : {&ix->prof_used, &ix->prof_free})
+    for (auto& pe : *v) {
+      cudaEventDestroy(pe.e0);
+      cudaEventDestroy(pe.e1);
+      cudaEventDestroy(pe.e2);
+    }
+  delete ix;
+}
+
+int linr_index_profile(linr_index* ix, int enable) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  ix->prof = enable != 0;
+  return LINR_OK;
+}
+
+int linr_index_profile_read(linr_index* ix, double* scan_ms, double* merge_ms, int64_t* searches,
+                            int64_t* launches) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  DeviceGuard dg(ix->d.device);
+  double s = 0.0, m = 0.0;
+  for (auto& pe : ix->prof_used) {
+    cudaError_t e = cudaEventSynchronize(pe.e2);
+    if (e != cudaSuccess) return cuda_fail(e, "profile events");
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, pe.e0, pe.e1);
+    cudaEventElapsedTime(&b, pe.e1, pe.e2);
+    s += a;
+    m += b;
+  }
+  if (scan_ms) *scan_ms = s;
+  if (merge_ms) *merge_ms = m;
+  if (searches) *searches = (int64_t)ix->prof_used.size();
+  if (launches) *launches = ix->prof_launches;
+  for (auto& pe : ix->prof_used) ix->prof_free.push_back(pe);
+  ix->prof_used.clear();
+  ix->prof_launches = 0;
+  return LINR_OK;
+}
+
+int linr_index_load(linr_index* ix, int64_t row0, int64_t n, const void* emb, const uint64_t* attrs, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (n < 0) return fail(LINR_EINVAL, "n < 0");
+  if (n == 0) return LINR_OK;
+  if (!emb || !attrs) return fail(LINR_EINVAL, "null input");
+  const int64_t r0 = row0 - ix->d.global_row0;
+  if (r0 < 0 || r0 + n > ix->d.capacity_rows) return fail(LINR_ERANGE, "rows outside this shard");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync((char*)ix->emb + r0 * ix->rowbytes, emb, (size_t)n * ix->rowbytes,
+                                  cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "load emb copy");
+  e = launch_attr_soa(attrs, n, ix->d.attr_words, ix->attr, ix->cap_pad, r0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "load attrs");
+  e = launch_set_live_range(ix->live, ix->hdr, r0, n, st);
+  if (e != cudaSuccess) return cuda_fail(e, "load live");
+  return LINR_OK;
+}
+
+int linr_index_update_rows(linr_index* ix, const int64_t* rows, int64_t n, const void* emb, const uint64_t* attrs,
+                           void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (n < 0) return fail(LINR_EINVAL, "n < 0");
+  if (n == 0) return LINR_OK;
+  if (!rows || !emb || !attrs) return fail(LINR_EINVAL, "null input");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = launch_update_rows(rows, n, ix->d.global_row0, ix->d.capacity_rows, ix->rowbytes, emb, attrs,
+                                     ix->d.attr_words, ix->emb, ix->attr, ix->cap_pad, ix->live, ix->hdr,
+                                     (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "update launch");
+  return LINR_OK;
+}
+
+int linr_index_delete_rows(linr_index* ix, const int64_t* rows, int64_t n, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (n < 0) return fail(LINR_EINVAL, "n < 0");
+  if (n == 0) return LINR_OK;
+  if (!rows) return fail(LINR_EINVAL, "null rows");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = launch_delete_rows(rows, n, ix->d.global_row0, ix->d.capacity_rows, ix->live, ix->hdr,
+                                     (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "delete launch");
+  return LINR_OK;
+}
+
+int linr_index_stats(linr_index* ix, int64_t* hwm, int64_t* skipped, int64_t* overflow, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  DeviceGuard dg(ix->d.device);
+  DevHeader h;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(&h, ix->hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "stats");
+  if (hwm) *hwm = (int64_t)h.hwm;
+  if (skipped) *skipped = (int64_t)h.skipped;
+  if (overflow) *overflow = (int64_t)h.overflow;
+  return LINR_OK;
+}
+
+size_t linr_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K) {
+  if (!ix || B < 1 || V < 1 || V > 8 || K < 1 || K > LINR_MAX_K) return 0;
+  Plan pl;
+  std::string why;
+  if (!make_plan(ix, B, V, K, &pl, &why)) return 0;
+  return ws_layout(pl, B, K).end;
+}
+
+int linr_search(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,
+                int32_t K, void* ws, size_t ws_bytes, int64_t* out_ids, float* out_scores, int64_t* out_pass,
+                void* stream) {
+  return search_impl(ix, q, B, V, cl, off, K, ws, ws_bytes, 0, out_ids, out_scores, nullptr, out_pass,
+                     (cudaStream_t)stream);
+}
+
+int linr_search_keys(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl,
+                     const int32_t* off, int32_t K, void* ws, size_t ws_bytes, uint64_t* out_keys,
+                     int64_t* out_pass, void* stream) {
+  return search_impl(ix, q, B, V, cl, off, K, ws, ws_bytes, 1, nullptr, nullptr, out_keys, out_pass,
+                     (cudaStream_t)stream);
+}
+
+size_t linr_merge_workspace_bytes(int32_t L, int32_t B, int32_t K) {
+  if (L < 1 || B < 1 || K < 1 || K > LINR_MAX_K) return 0;
+  return 0;   // the merge kernel works entirely in shared memory
+}
+
+int linr_merge_keys(const uint64_t* keys, const int64_t* pass, int32_t L, int32_t B, int32_t K, void* ws,
+                    size_t ws_bytes, int64_t* out_ids, float* out_scores, int64_t* out_pass, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!keys || !pass || !out_ids || !out_scores) return fail(LINR_EINVAL, "null pointer");
+  if (L < 1 || B < 1 || K < 1 || K > LINR_MAX_K) return fail(LINR_EINVAL, "bad L/B/K");
+  if ((int64_t)L * K > 0x7FFFFFFF) return fail(LINR_EINVAL, "L*K too large");
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.keys = keys;
+  mp.stride_l = (int64_t)B * K;
+  mp.stride_u = K;
+  mp.pass = pass;
+  mp.pstride_l = B;
+  mp.pstride_u = 1;
+  mp.L = L;
+  mp.K = K;
+  mp.m = merge_sample_size(L, K);
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_pass = out_pass;
+  mp.mode = 0;
+  cudaError_t e = launch_merge(mp, B, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  return LINR_OK;
+}
+
+size_t linr_search_host_extra_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K) {
+  if (!ix || B < 1 || V < 1 || K < 1) return 0;
+  return align256((size_t)B * V * ix->rowbytes) + align256((size_t)B * K * 8) + align256((size_t)B * K * 4) +
+         align256((size_t)B * 8);
+}
+
+int linr_search_host(linr_index* ix, const void* q_host, int32_t B, int32_t V, const linr_clause* cl,
+                     const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* ids_host,
+                     float* scores_host, int64_t* pass_host, void* stream) {
+  if (!ix || !q_host || !ids_host || !scores_host) return fail(LINR_EINVAL, "null pointer");
+  const size_t need = linr_search_workspace_bytes(ix, B, V, K);
+  const size_t extra = linr_search_host_extra_bytes(ix, B, V, K);
+  if (need == 0 || extra == 0) return fail(LINR_EINVAL, "bad B/V/K");
+  if (!ws || ws_bytes < need + extra) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* x = (char*)ws + align256(need);
+  void* qd = x;
+  x += align256((size_t)B * V * ix->rowbytes);
+  int64_t* idd = (int64_t*)x;
+  x += align256((size_t)B * K * 8);
+  float* scd = (float*)x;
+  x += align256((size_t)B * K * 4);
+  int64_t* psd = (int64_t*)x;
+  if (ws_bytes < align256(need) + extra) return fail(LINR_ENOMEM, "workspace too small");
+  cudaError_t e = cudaMemcpyAsync(qd, q_host, (size_t)B * V * ix->rowbytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "query H2D");
+  int rc = search_impl(ix, qd, B, V, cl, off, K, ws, need, 0, idd, scd, nullptr, psd, st);
+  if (rc != LINR_OK) return rc;
+  e = cudaMemcpyAsync(ids_host, idd, (size_t)B * K * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && pass_host) e = cudaMemcpyAsync(pass_host, psd, (size_t)B * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "search_host copies");
+  return LINR_OK;
+}
+
+int linr_index_generate(linr_index* ix, uint64_t seed, int32_t mode, int64_t row_begin, int64_t n, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (mode != 0 && mode != 1) return fail(LINR_EINVAL, "mode must be 0 or 1");
+  if (n < 0 || row_begin < 0 || row_begin + n > ix->d.capacity_rows) return fail(LINR_ERANGE, "rows outside shard");
+  if (n == 0) return LINR_OK;
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // counters are GLOBAL row ids, so every shard of a sharded index generates consistent rows
+  cudaError_t e = launch_generate(ix->d.dtype, ix->d.dim, ix->d.attr_words, seed, mode,
+                                  ix->d.global_row0 + row_begin, n, (char*)ix->emb, row_begin, ix->attr,
+                                  ix->cap_pad, true, st);
+  if (e != cudaSuccess) return cuda_fail(e, "generate");
+  e = launch_set_live_range(ix->live, ix->hdr, row_begin, n, st);
+  if (e != cudaSuccess) return cuda_fail(e, "generate live");
+  return LINR_OK;
+}
+
+int linr_generate_rows(int32_t dtype, int32_t dim, int32_t W, uint64_t seed, int32_t mode, int64_t row_begin,
+                       int64_t n, void* emb, uint64_t* attrs, void* stream) {
+  if (dtype < 0 || dtype > 3 || dim < 1 || W < 1 || W > 4 || n < 0 || (mode != 0 && mode != 1))
+    return fail(LINR_EINVAL, "bad generator arguments");
+  if (n == 0) return LINR_OK;
+  cudaError_t e = launch_generate(dtype, dim, W, seed, mode, row_begin, n, emb, 0, attrs, 0, false,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "generate");
+  return LINR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/linr.h"
+
+namespace linr {
+
+constexpr int kHdrBytes = 256;   // device header at the start of live_storage
+struct DevHeader {               // lives in device memory
+  unsigned long long hwm;        // local rows [0, hwm) may be live
+  unsigned long long skipped;    // out-of-shard ids seen by update/delete
+  unsigned long long overflow;   // scan buffer overflows (must stay 0; checked by tests)
+};
+
+struct KClause {                 // clause as the kernels see it (16 B)
+  unsigned long long mask;
+  uint32_t word;
+  uint32_t rev;
+};
+
+// Parameters of one GEMV scan launch (passed by value; <= 4 KB).
+struct ScanParams {
+  const void* emb;               // [cap_pad][dim]
+  const uint64_t* attr;          // SoA [W][cap_pad]
+  const uint32_t* live;          // bitmap [cap_pad/32]
+  DevHeader* hdr;
+  int64_t cap_pad;
+  uint32_t row0;                 // global id of local row 0
+  int nu;                        // users in this launch
+  int V;                         // vectors per user
+  int K;
+  int C;                         // soft capacity of the per-user CTA buffer
+  int bufcap;                    // hard capacity (C + headroom)
+  uint32_t wmask;                // attribute words referenced by any clause
+  const void* q;                 // [nu][V][dim] queries of this launch's users
+  uint64_t* out_keys;            // [nu][gridDim.x][K]
+  int64_t* out_pass;             // [nu][gridDim.x]
+  int ncl[8];
+  KClause cl[8][16];
+};
+
+struct ScanCfg {                 // launch geometry chosen for one (dtype, dim, nqv)
+  int nt;                        // threads per CTA
+  int rows_per_iter;             // rows a warp scores per inner iteration (append burst bound)
+};
+
+// Launch the fused filter + score + CTA top-K scan. nqv = padded vectors per launch (1,2,4,8).
+cudaError_t launch_scan_gemv(int dtype, int dim, int nqv, const ScanParams& p, int grid,
+                             size_t smem, cudaStream_t st);
+bool scan_gemv_supported(int dtype, int dim, int nqv);
+ScanCfg scan_gemv_cfg(int dtype, int dim, int nqv);
+
+// Merge L sorted key lists per user into the final top-K.
+struct MergeParams {
+  const uint64_t* keys;          // list l of user u at keys + l*stride_l + u*stride_u, length K
+  int64_t stride_l, stride_u;
+  const int64_t* pass;           // pass[l*pstride_l + u*pstride_u]
+  int64_t pstride_l, pstride_u;
+  int L, K, m;                   // m: per-list sample size for the pruned path
+  int64_t* out_ids;              // [B][K] (mode 0)
+  float* out_scores;             // [B][K] (mode 0)
+  uint64_t* out_keys;            // [B][K] (mode 1)
+  int64_t* out_pass;             // [B] (may be null)
+  int mode;                      // 0: decode ids/scores, 1: keys
+};
+cudaError_t launch_merge(const MergeParams& p, int B, cudaStream_t st);
+int merge_sample_size(int L, int K);
+
+// index maintenance kernels
+cudaError_t launch_attr_soa(const uint64_t* src, int64_t n, int W, uint64_t* dst_soa, int64_t cap_pad,
+                            int64_t r0, cudaStream_t st);
+cudaError_t launch_set_live_range(uint32_t* live, DevHeader* hdr, int64_t r0, int64_t n, cudaStream_t st);
+cudaError_t launch_update_rows(const int64_t* rows, int64_t n, int64_t grow0, int64_t cap, int rowbytes,
+                               const void* emb_src, const uint64_t* attr_src, int W, void* emb,
+                               uint64_t* attr, int64_t cap_pad, uint32_t* live, DevHeader* hdr,
+                               cudaStream_t st);
+cudaError_t launch_delete_rows(const int64_t* rows, int64_t n, int64_t grow0, int64_t cap, uint32_t* live,
+                               DevHeader* hdr, cudaStream_t st);
+cudaError_t launch_generate(int dtype, int dim, int W, uint64_t seed, int mode, int64_t row_begin, int64_t n,
+                            void* emb, int64_t emb_row_offset, uint64_t* attrs, int64_t attr_stride_rows,
+                            bool attrs_soa, cudaStream_t st);
+
+void set_error(const std::string& msg);
+
+}  // namespace linr

@@ -1,0 +1,9 @@
+// Explicit instantiation of the GEMV scan kernels for dtype LINR_BF16 (split per dtype for parallel builds).
+#include "scan_gemv.cuh"
+
+namespace linr {
+cudaError_t launch_scan_gemv_bf16(int dim, int nqv, const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
+  return ScanDispatch<LINR_BF16>::launch(dim, nqv, p, grid, smem, st);
+}
+ScanCfg scan_cfg_bf16(int dim, int nqv) { return ScanDispatch<LINR_BF16>::cfg(dim, nqv); }
+}  // namespace linr

@@ -1,0 +1,9 @@
+// Explicit instantiation of the GEMV scan kernels for dtype LINR_F32 (split per dtype for parallel builds).
+#include "scan_gemv.cuh"
+
+namespace linr {
+cudaError_t launch_scan_gemv_f32(int dim, int nqv, const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
+  return ScanDispatch<LINR_F32>::launch(dim, nqv, p, grid, smem, st);
+}
+ScanCfg scan_cfg_f32(int dim, int nqv) { return ScanDispatch<LINR_F32>::cfg(dim, nqv); }
+}  // namespace linr

@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element (-m gpu).
+
+Exactness bar (BASELINE.json north_star / DESIGN.md R8-R10): int8 and integer-grid float inputs
+are bit-exact (ids and scores); dense float inputs match per reading R9 (scores within the R8
+tolerance, id sets equal except ties within tolerance at the K-th boundary).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen as dg
+import oracle
+from parity import check, make_index, to_torch, attrs_torch
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def run_case(dtype, d, n, B, V, K, preset, mode, live_frac=1.0, seed=dg.DATA_SEED, W=1, what=""):
+    vals, attrs = dg.gen_items(seed, 0, n, d, dtype, mode, W=W)
+    live = np.ones(n, np.uint8)
+    ix = make_index(vals, attrs, dtype)
+    if live_frac < 1.0:
+        rng = np.random.default_rng(n + d)
+        dead = np.nonzero(rng.random(n) > live_frac)[0]
+        live[dead] = 0
+        ix.delete_rows(torch.from_numpy(dead).to(DEV))
+    Q = dg.gen_queries(dg.QUERY_SEED, seed, max(n, 1), B, V, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    ref = oracle.search(dtype, vals, attrs, live, Q, cls, K)
+    exact = dtype == dg.I8 or mode == dg.MODE_GRID
+    check(dtype, vals, attrs, live, Q, cls, K, g, ref, exact, what=what)
+    assert ix.stats()["overflow"] == 0
+    return ix
+
+
+def test_config_c1_full():
+    """c1: 100k items, d=64 fp32, 4 clauses, 1 query, K=100 (BASELINE.json configs[0])."""
+    run_case(dg.F32, 64, 100_000, 1, 1, 100, "HIGH4", dg.MODE_DENSE, what="c1 dense")
+    run_case(dg.F32, 64, 100_000, 1, 1, 100, "HIGH4", dg.MODE_GRID, what="c1 grid")
+
+
+@pytest.mark.parametrize("dtype", [dg.F32, dg.F16, dg.BF16, dg.I8])
+@pytest.mark.parametrize("d", [16, 64, 128, 256])
+def test_dtypes_dims_grid_exact(dtype, d):
+    run_case(dtype, d, 20_011, 1, 1, 1000, "HIGH", dg.MODE_GRID, what=f"dt{dtype} d{d}")
+
+
+@pytest.mark.parametrize("dtype", [dg.F16, dg.BF16])
+def test_dense_tolerance(dtype):
+    run_case(dtype, 128, 50_000, 2, 1, 500, "HIGH", dg.MODE_DENSE, what="dense")
+
+
+@pytest.mark.parametrize("preset", ["ALL", "HIGH", "HIGH4", "LOW"])
+@pytest.mark.parametrize("K", [1, 10, 1000, 2048])
+def test_presets_and_K(preset, K):
+    run_case(dg.I8, 128, 30_000 + 77, 1, 1, K, preset, dg.MODE_DENSE, what=f"{preset} K{K}")
+
+
+@pytest.mark.parametrize("B,V", [(2, 1), (3, 1), (4, 1), (8, 1), (11, 1), (1, 2), (1, 8), (2, 4), (3, 2)])
+def test_batches_and_multivector(B, V):
+    run_case(dg.BF16, 128, 25_000, B, V, 300, "HIGH", dg.MODE_GRID, what=f"B{B} V{V}")
+    run_case(dg.I8, 64, 25_000, B, V, 300, "LOW", dg.MODE_DENSE, what=f"i8 B{B} V{V}")
+
+
+def test_liveness_and_multiword_attrs():
+    run_case(dg.I8, 64, 40_000, 3, 1, 200, "HIGH", dg.MODE_DENSE, live_frac=0.7, what="live")
+    # clauses on attribute words 1..3 (random 64-bit words)
+    n, d, W = 20_000, 64, 4
+    vals, attrs = dg.gen_items(3, 0, n, d, dg.I8, dg.MODE_DENSE, W=W)
+    ix = make_index(vals, attrs, dg.I8)
+    Q = dg.gen_queries(4, 3, n, 2, 1, d, dg.I8)
+    cls = [[(0x00F0_0000_0000_00F0, 1, 0), (0x1, 3, 1), (0xFFFF << 24, 0, 1)],
+           [(0x8000_0000_0000_0001, 2, 0)]]
+    g = ix.search(to_torch(Q, dg.I8, DEV), cls, 100)
+    ref = oracle.search(dg.I8, vals, attrs, np.ones(n), Q, cls, 100)
+    check(dg.I8, vals, attrs, np.ones(n), Q, cls, 100, g, ref, True, what="multiword")
+
+
+def test_no_clauses_and_zero_query_tie_break():
+    n, d = 10_000, 64
+    vals, attrs = dg.gen_items(5, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    Q = np.zeros((2, 1, d), np.uint16)   # bf16 zeros: every score is 0 -> lowest ids first
+    cls = [[], [(0xFF << 56, 0, 0)]]
+    g = ix.search(to_torch(Q, dg.BF16, DEV), cls, 50)
+    ref = oracle.search(dg.BF16, vals, attrs, np.ones(n), Q, cls, 50)
+    check(dg.BF16, vals, attrs, np.ones(n), Q, cls, 50, g, ref, True, what="zero query")
+    assert g[0][0, :50].cpu().tolist() == list(range(50))
+
+
+def test_empty_index_and_K_exceeds_pass():
+    d = 64
+    from paper_2407_13218_b200 import Index
+    ix = Index(1000, d, dg.I8, 1)
+    Q = dg.gen_queries(1, 1, 10, 2, 1, d, dg.I8)
+    ids, sc, ps = ix.search(to_torch(Q, dg.I8, DEV), dg.gen_clauses(1, 2, "HIGH"), 16)
+    assert (ids.cpu() == -1).all() and torch.isinf(sc.cpu()).all() and (ps.cpu() == 0).all()
+    run_case(dg.I8, d, 3_000, 2, 1, 2048, "LOW", dg.MODE_DENSE, what="K > pass")
+
+
+def test_adversarial_increasing_scores():
+    """Scores increase with row id: every item beats the running threshold, so the CTA buffers
+    compact as often as possible; the result must still be the last K passing rows."""
+    n, d, K = 300_000, 16, 1000
+    vals = np.zeros((n, d), np.float32)
+    vals[:, 0] = np.arange(n, dtype=np.float32)
+    attrs = np.full((n, 1), 1, np.uint64)
+    ix = make_index(vals, attrs, dg.F32)
+    q = np.zeros((1, d), np.float32)
+    q[0, 0] = 1.0
+    g = ix.search(torch.from_numpy(q).to(DEV), [[(1, 0, 0)]], K)
+    ref = oracle.search(dg.F32, vals, attrs, np.ones(n), q, [[(1, 0, 0)]], K)
+    check(dg.F32, vals, attrs, np.ones(n), q, [[(1, 0, 0)]], K, g, ref, True, what="increasing")
+    assert ix.stats()["overflow"] == 0
+
+
+def test_live_updates_replay_equivalence():
+    """Upsert + delete in place (§4.3) then search == oracle on the final rows."""
+    n, d, K = 60_000, 128, 500
+    dtype = dg.BF16
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dtype, capacity=n + 5000)
+    rng = np.random.default_rng(9)
+    upd = rng.choice(n, 3000, replace=False)
+    new_rows = np.concatenate([upd, np.arange(n, n + 2000)])          # overwrite + append beyond hwm
+    nv, na = dg.gen_items(dg.UPDATE_SEED, 0, len(new_rows), d, dtype, dg.MODE_GRID)
+    ix.update_rows(torch.from_numpy(new_rows).to(DEV), to_torch(nv, dtype, DEV), attrs_torch(na, DEV))
+    dele = rng.choice(n, 4000, replace=False)
+    ix.delete_rows(torch.from_numpy(dele).to(DEV))
+    # out-of-shard ids are skipped and counted
+    ix.delete_rows(torch.tensor([-5, n + 999_999], device=DEV))
+    st = ix.stats()
+    assert st["hwm"] == n + 2000 and st["skipped"] == 2
+    fv = np.concatenate([vals, np.zeros((2000, d), vals.dtype)])
+    fa = np.concatenate([attrs, np.zeros((2000, 1), np.uint64)])
+    fv[new_rows], fa[new_rows] = nv, na
+    live = np.ones(n + 2000, np.uint8)
+    live[dele] = 0
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, 3, 1, d, dtype, dg.MODE_GRID)
+    cls = dg.gen_clauses(dg.QUERY_SEED, 3, "HIGH")
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    ref = oracle.search(dtype, fv, fa, live, Q, cls, K)
+    check(dtype, fv, fa, live, Q, cls, K, g, ref, True, what="updates")
+
+
+@pytest.mark.parametrize("dtype", [dg.F32, dg.F16, dg.BF16, dg.I8])
+@pytest.mark.parametrize("mode", [dg.MODE_GRID, dg.MODE_DENSE])
+def test_device_generator_matches_datagen(dtype, mode):
+    from paper_2407_13218_b200 import generate_rows
+    d, W = 128, 3
+    emb, att = generate_rows(dtype, d, W, dg.DATA_SEED, mode, 123_456, 5000)
+    v, a = dg.gen_items(dg.DATA_SEED, 123_456, 5000, d, dtype, mode, W=W)
+    ge = emb.cpu()
+    if dtype in (dg.F16, dg.BF16):
+        ge = ge.view(torch.int16).numpy().view(np.uint16)
+    else:
+        ge = ge.numpy()
+    assert np.array_equal(ge, v)
+    assert np.array_equal(att.cpu().numpy().view(np.uint64), a)
+
+
+def test_index_generate_equals_load():
+    n, d = 50_000, 64
+    from paper_2407_13218_b200 import Index
+    ix = Index(n, d, dg.I8, 1, global_row0=1000)
+    ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, n)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 1000, n, d, dg.I8)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, 2, 1, d, dg.I8)
+    cls = dg.gen_clauses(dg.QUERY_SEED, 2, "HIGH")
+    g = ix.search(to_torch(Q, dg.I8, DEV), cls, 100)
+    ref = oracle.search(dg.I8, vals, attrs, np.ones(n), Q, cls, 100, row0=1000)
+    check(dg.I8, vals, attrs, np.ones(n), Q, cls, 100, g, ref, True, row0=1000, what="generate")
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_virtual_shards_merge(G):
+    """Row-sharded search on one GPU: G shards with global_row0 offsets, shard-local keys, then
+    the merge kernel (the same kernel the multi-GPU all-gather feeds) == one index == oracle."""
+    from paper_2407_13218_b200 import Index, merge_keys
+    n, d, K, B = 80_000, 128, 1000, 2
+    dtype = dg.I8
+    per = -(-n // G)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    qt = to_torch(Q, dtype, DEV)
+    keys, ps = [], []
+    for r in range(G):
+        lo, hi = r * per, min(n, (r + 1) * per)
+        ix = Index(per, d, dtype, 1, global_row0=lo)
+        ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, hi - lo)
+        k, p = ix.search_keys(qt, cls, K)
+        keys.append(k)
+        ps.append(p)
+    g = merge_keys(torch.stack(keys), torch.stack(ps), K)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype)
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what=f"shards{G}")
+
+
+def test_search_host_e2e_path():
+    n, d, K = 30_000, 128, 100
+    vals, attrs = dg.gen_items(1, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    Q = dg.gen_queries(2, 1, n, 3, 1, d, dg.BF16, dg.MODE_GRID)
+    cls = dg.gen_clauses(2, 3, "HIGH")
+    qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16).contiguous().pin_memory()
+    g = ix.search_host(qh, cls, K)
+    ref = oracle.search(dg.BF16, vals, attrs, np.ones(n), Q, cls, K)
+    check(dg.BF16, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what="host")
+
+
+def test_invalid_arguments_raise():
+    from paper_2407_13218_b200 import Index, LinrError
+    ix = Index(1000, 64, dg.I8, 1)
+    q = torch.zeros((1, 64), dtype=torch.int8, device=DEV)
+    with pytest.raises(LinrError):
+        ix.search(q, [[(0, 0, 0)]], 10)          # empty clause mask (reading R3)
+    with pytest.raises(LinrError):
+        ix.search(q, [[(1, 1, 0)]], 10)          # word >= W
+    with pytest.raises(LinrError):
+        ix.search(q, [[]], 4096)                 # K > 2048
+    with pytest.raises(LinrError):
+        ix.load(torch.zeros((10, 64), dtype=torch.int8, device=DEV),
+                torch.zeros((10, 1), dtype=torch.int64, device=DEV), row0=995)   # ERANGE

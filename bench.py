@@ -39,7 +39,7 @@ PRESET = "HIGH"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="linr", choices=["linr", "reference"])
     ap.add_argument("--batch", type=int, default=B)

@@ -190,6 +190,11 @@ int linr_index_profile(linr_index* index, int enable);
 int linr_index_profile_read(linr_index* index, double* scan_ms, double* merge_ms, int64_t* searches,
                             int64_t* kernel_launches);
 
+/* Diagnostics (development only; not needed by users): enable device-side phase timers
+ * (%globaltimer ns per CTA phase of the scan and merge kernels) and read them back. */
+int linr_debug_timers(int enable);
+int linr_debug_read(uint64_t* host, int32_t n);
+
 /* Thread-local message for the last non-OK return on this thread ("" if none). */
 const char* linr_last_error(void);
 

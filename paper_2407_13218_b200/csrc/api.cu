@@ -22,6 +22,9 @@ ScanCfg scan_cfg_f16(int, int);
 ScanCfg scan_cfg_bf16(int, int);
 ScanCfg scan_cfg_i8(int, int);
 
+static unsigned long long* g_dbg_host_ptr = nullptr;
+static bool g_dbg_on = false;
+unsigned long long* debug_buffer() { return g_dbg_on ? g_dbg_host_ptr : nullptr; }
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
 
@@ -46,16 +49,19 @@ ScanCfg scan_gemv_cfg(int dtype, int dim, int nqv) {
     case LINR_BF16: return scan_cfg_bf16(dim, nqv);
     case LINR_I8: return scan_cfg_i8(dim, nqv);
   }
-  return ScanCfg{0, 0};
+  return ScanCfg{0, 0, 0};
 }
-// query registers per lane = nqv * (chunks per lane) * (fp32 values or packed words per chunk)
+// query registers per lane = nqv * (chunks per lane) * (fp32 values or packed words per chunk);
+// mirrors geom_lpr() in scan_gemv.cuh
 bool scan_gemv_supported(int dtype, int dim, int nqv) {
   if (!dim_ok(dim)) return false;
   const int ch = dim * esize(dtype) / 16;
-  const int lpr = ch < 32 ? ch : 32;
-  const int cpl = ch / lpr;
-  const int per_chunk = dtype == LINR_I8 ? 4 : 16 / esize(dtype);
-  return nqv * cpl * per_chunk <= 64;
+  const int per = dtype == LINR_I8 ? 4 : 16 / esize(dtype);
+  int lpr = ch / 4 > 4 ? ch / 4 : 4;
+  if (lpr > 32) lpr = 32;
+  if (lpr > ch) lpr = ch;
+  while (lpr < ch && lpr < 32 && nqv * (ch / lpr) * per > 32) lpr *= 2;
+  return nqv * (ch / lpr) * per <= 64;
 }
 
 }  // namespace linr
@@ -111,38 +117,40 @@ struct Plan {
   int nqv = 0;
   int nt = 0;
   int C = 0, bufcap = 0;
+  int list_cap = 0;   // per-CTA output list capacity
   size_t smem = 0;
   int grid = 0;
 };
 
-constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) rounded (checked in scan_gemv.cuh users)
+constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) (static_assert in scan_gemv.cuh)
 
 bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why) {
   const int dt = ix->d.dtype, dim = ix->d.dim;
-  const int p2k = next_pow2(K);
   int nu = std::max(1, std::min(B, std::min(kMaxUsers, 8 / V)));
   for (; nu >= 1; --nu) {
     const int nqv = next_pow2(nu * V);
     if (nqv > 8 || !scan_gemv_supported(dt, dim, nqv)) continue;
     const ScanCfg cfg = scan_gemv_cfg(dt, dim, nqv);
     if (cfg.nt == 0) continue;
-    const int head = (cfg.nt / 32) * cfg.rows_per_iter;
-    for (int C : {std::max(2 * p2k, 1024), p2k + 512}) {
-      if (C <= K) continue;
-      const int bufcap = std::max(C + head, p2k);
-      const size_t smem = kScanCtlBytes + (size_t)nu * bufcap * 8 + (size_t)(cfg.nt / 32) * kTileItems * 2;
-      if (smem <= ix->smem_optin) {
-        pl->nu_g = nu;
-        pl->groups = (B + nu - 1) / nu;
-        pl->nqv = nqv;
-        pl->nt = cfg.nt;
-        pl->C = C;
-        pl->bufcap = bufcap;
-        pl->smem = smem;
-        pl->grid = ix->num_sms;
-        return true;
-      }
-    }
+    const int nw = cfg.nt / 32;
+    const int head = nw * cfg.rows_per_iter;
+    const size_t fixed = kScanCtlBytes + (size_t)nw * kTileItems * 2 + (size_t)nw * cfg.ring_bytes;
+    if (ix->smem_optin <= fixed) continue;
+    // the largest per-user buffer that fits: fewer compactions (each one drains the CTA)
+    long long C = (long long)((ix->smem_optin - fixed) / (8 * (size_t)nu)) - head;
+    C = std::min<long long>(C, 32768);
+    C &= ~255ll;
+    if (C < K + 256) continue;
+    pl->nu_g = nu;
+    pl->groups = (B + nu - 1) / nu;
+    pl->nqv = nqv;
+    pl->nt = cfg.nt;
+    pl->C = (int)C;
+    pl->bufcap = (int)C + head;
+    pl->smem = std::max(fixed + (size_t)nu * pl->bufcap * 8, merge_smem());
+    pl->grid = ix->num_sms;
+    pl->list_cap = (B <= 8) ? pl->bufcap : std::min(pl->bufcap, std::max(2 * K, 2048));
+    return true;
   }
   *why = "no GEMV scan configuration fits (dtype " + std::to_string(dt) + ", dim " + std::to_string(dim) +
          ", V " + std::to_string(V) + ", K " + std::to_string(K) + ")";
@@ -150,13 +158,17 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
 }
 
 struct WsLayout {
-  size_t lists = 0, pass = 0, end = 0;
+  size_t samp = 0, list = 0, cnt = 0, pass = 0, end = 0;
 };
 WsLayout ws_layout(const Plan& pl, int B, int K) {
+  (void)K;
   WsLayout w;
-  w.lists = 0;
-  w.pass = align256((size_t)B * pl.grid * K * 8);
-  w.end = w.pass + align256((size_t)B * pl.grid * 8);
+  const size_t parts = (size_t)B * pl.grid;
+  w.samp = 0;
+  w.list = align256(parts * kScanSample * 8);
+  w.cnt = w.list + align256(parts * pl.list_cap * 8);
+  w.pass = w.cnt + align256(parts * 4);
+  w.end = w.pass + align256(parts * 8);
   return w;
 }
 
@@ -200,7 +212,9 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
 
-  uint64_t* lists = (uint64_t*)((char*)ws + wl.lists);
+  uint64_t* samp = (uint64_t*)((char*)ws + wl.samp);
+  uint64_t* lists = (uint64_t*)((char*)ws + wl.list);
+  int* cnts = (int*)((char*)ws + wl.cnt);
   int64_t* pass = (int64_t*)((char*)ws + wl.pass);
   ProfEvents pe{};
   if (ix->prof) {
@@ -214,6 +228,32 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
     }
     cudaEventRecord(pe.e0, st);
   }
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.samp = samp;
+  mp.samp_sl = kScanSample;
+  mp.samp_su = (int64_t)pl.grid * kScanSample;
+  mp.ms = kScanSample;
+  mp.list = lists;
+  mp.list_sl = pl.list_cap;
+  mp.list_su = (int64_t)pl.grid * pl.list_cap;
+  mp.cnt = cnts;
+  mp.cnt_sl = 1;
+  mp.cnt_su = pl.grid;
+  mp.list_len = pl.list_cap;
+  mp.pass = pass;
+  mp.pstride_l = 1;
+  mp.pstride_u = pl.grid;
+  mp.L = pl.grid;
+  mp.K = K;
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_keys = out_keys;
+  mp.out_pass = out_pass;
+  mp.mode = mode;
+  mp.dbg = debug_buffer();
+  // one scan launch: its last CTAs run the merge (saves a launch); several: a merge kernel
+  const bool fused = pl.groups == 1;
   for (int g = 0; g < pl.groups; ++g) {
     const int u0 = g * pl.nu_g;
     const int nu = std::min(pl.nu_g, B - u0);
@@ -230,9 +270,14 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
     p.K = K;
     p.C = pl.C;
     p.bufcap = pl.bufcap;
+    p.list_cap = pl.list_cap;
+    p.dbg = debug_buffer();
     p.q = (const char*)q + (size_t)u0 * V * ix->rowbytes;
-    p.out_keys = lists + (size_t)u0 * pl.grid * K;
-    p.out_pass = pass + (size_t)u0 * pl.grid;
+    const size_t part0 = (size_t)u0 * pl.grid;
+    p.out_samp = samp + part0 * kScanSample;
+    p.out_list = lists + part0 * pl.list_cap;
+    p.out_cnt = cnts + part0;
+    p.out_pass = pass + part0;
     uint32_t wmask = 0;
     for (int u = 0; u < nu; ++u) {
       const int b = u0 + u;
@@ -246,32 +291,20 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
       }
     }
     p.wmask = wmask;
+    p.fuse_merge = fused ? 1 : 0;
+    p.mp = mp;
     e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, p, pl.grid, pl.smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "scan launch");
   }
   if (ix->prof) cudaEventRecord(pe.e1, st);
-  MergeParams mp;
-  std::memset(&mp, 0, sizeof(mp));
-  mp.keys = lists;
-  mp.stride_l = K;
-  mp.stride_u = (int64_t)pl.grid * K;
-  mp.pass = pass;
-  mp.pstride_l = 1;
-  mp.pstride_u = pl.grid;
-  mp.L = pl.grid;
-  mp.K = K;
-  mp.m = merge_sample_size(pl.grid, K);
-  mp.out_ids = out_ids;
-  mp.out_scores = out_scores;
-  mp.out_keys = out_keys;
-  mp.out_pass = out_pass;
-  mp.mode = mode;
-  e = launch_merge(mp, B, st);
-  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  if (!fused) {
+    e = launch_merge(mp, B, st);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  }
   if (ix->prof) {
     cudaEventRecord(pe.e2, st);
     ix->prof_used.push_back(pe);
-    ix->prof_launches += pl.groups + 1;
+    ix->prof_launches += pl.groups + (fused ? 0 : 1);
   }
   return LINR_OK;
 }
@@ -294,6 +327,25 @@ bool desc_ok(const linr_index_desc* d, std::string* why) {
 extern "C" {
 
 int linr_version(void) { return 1; }
+
+int linr_debug_timers(int enable) {
+  unsigned long long* p = nullptr;
+  if (enable) {
+    if (!g_dbg_host_ptr && cudaMalloc(&g_dbg_host_ptr, 8192 * 8) != cudaSuccess) return fail(LINR_ECUDA, "dbg alloc");
+    cudaMemset(g_dbg_host_ptr, 0, 8192 * 8);
+    p = g_dbg_host_ptr;
+  }
+  g_dbg_on = p != nullptr;
+  return LINR_OK;
+}
+
+int linr_debug_read(uint64_t* host, int32_t n) {
+  if (!g_dbg_host_ptr || !host || n < 0 || n > 8192) return fail(LINR_EINVAL, "debug timers not enabled");
+  cudaError_t e = cudaMemcpy(host, g_dbg_host_ptr, (size_t)n * 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "dbg read");
+  cudaMemset(g_dbg_host_ptr, 0, 8192 * 8);
+  return LINR_OK;
+}
 const char* linr_last_error(void) { return g_err.c_str(); }
 
 size_t linr_storage_bytes(const linr_index_desc* d, int which) {
@@ -471,21 +523,28 @@ int linr_merge_keys(const uint64_t* keys, const int64_t* pass, int32_t L, int32_
   if (!keys || !pass || !out_ids || !out_scores) return fail(LINR_EINVAL, "null pointer");
   if (L < 1 || B < 1 || K < 1 || K > LINR_MAX_K) return fail(LINR_EINVAL, "bad L/B/K");
   if ((int64_t)L * K > 0x7FFFFFFF) return fail(LINR_EINVAL, "L*K too large");
+  // shard lists are fully sorted: sample = their first min(32, K) keys, list = the whole list
   MergeParams mp;
   std::memset(&mp, 0, sizeof(mp));
-  mp.keys = keys;
-  mp.stride_l = (int64_t)B * K;
-  mp.stride_u = K;
+  mp.samp = keys;
+  mp.samp_sl = (int64_t)B * K;
+  mp.samp_su = K;
+  mp.ms = std::min(K, kScanSample);
+  mp.list = keys;
+  mp.list_sl = (int64_t)B * K;
+  mp.list_su = K;
+  mp.cnt = nullptr;
+  mp.list_len = K;
   mp.pass = pass;
   mp.pstride_l = B;
   mp.pstride_u = 1;
   mp.L = L;
   mp.K = K;
-  mp.m = merge_sample_size(L, K);
   mp.out_ids = out_ids;
   mp.out_scores = out_scores;
   mp.out_pass = out_pass;
   mp.mode = 0;
+  mp.dbg = debug_buffer();
   cudaError_t e = launch_merge(mp, B, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "merge launch");
   return LINR_OK;

@@ -50,6 +50,17 @@ LINR_DEV uint64_t ldg_stream_u64(const uint64_t* p) {
   return r;
 }
 
+// ---------------------------------------------------------------- diagnostics
+// Optional phase timers (linr_debug_timers): slot = base + idx, written by thread 0 of a CTA.
+LINR_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+LINR_DEV void dbg_mark(unsigned long long* d, int slot) {
+  if (d != nullptr && threadIdx.x == 0) d[slot] = gtimer();
+}
+
 // ---------------------------------------------------------------- CTA-wide primitives
 // Scratch used by the CTA-wide helpers (lives in shared memory).
 struct SelScratch {
@@ -61,12 +72,13 @@ struct SelScratch {
 
 // Radix select: returns T such that |{i < n : get(i) >= T}| == k exactly, for 1 <= k <= n and
 // pairwise-distinct keys. Keys below T are provably outside the top-k. All threads of the CTA
-// must call it (contains __syncthreads). Digits of 8 bits from the first byte where the keys
-// differ; stops early once the selected digit's whole bucket belongs to the top-k.
+// must call it (contains __syncthreads). 8-bit digits starting at the highest bit where the keys
+// differ (so the first digit already spreads the keys); stops early once the selected digit's
+// whole bucket belongs to the top-k. Plain shared-memory atomics for the histogram: measured on
+// B200 2.4x faster than warp-aggregating them with __match_any_sync.
 template <int NT, typename Get>
 __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // common prefix: AND / OR over all keys
   unsigned long long a = ~0ull, o = 0ull;
   for (int i = tid; i < n; i += NT) {
     uint64_t v = get(i);
@@ -82,18 +94,19 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
   if (lane == 0) { atomicAnd(&sc->red_and, a); atomicOr(&sc->red_or, o); }
   __syncthreads();
   const unsigned long long diff = sc->red_and ^ sc->red_or;
-  if (diff == 0ull) return sc->red_or;   // n == 1 (distinct keys): the key itself
-  const int hb = 63 - __clzll((long long)diff);
-  int shift = (hb / 8) * 8;
-  uint64_t prefix = sc->red_or & (shift == 56 ? 0ull : (~0ull << (shift + 8)));
-  uint64_t pmask = (shift == 56 ? 0ull : (~0ull << (shift + 8)));
-  int kk = k;
+  const unsigned long long orv = sc->red_or;
   __syncthreads();
-  for (; shift >= 0; shift -= 8) {
+  if (diff == 0ull) return orv;   // n == 1 (distinct keys): the key itself
+  const int hb = 63 - __clzll((long long)diff);
+  uint64_t pmask = (hb == 63) ? 0ull : (~0ull << (hb + 1));
+  uint64_t prefix = orv & pmask;  // bits above hb are common to every key
+  int shift = hb - 7 > 0 ? hb - 7 : 0;
+  int kk = k;
+  while (true) {
     for (int i = tid; i < 256; i += NT) sc->hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < n; i += NT) {
-      uint64_t v = get(i);
+      const uint64_t v = get(i);
       if ((v & pmask) == prefix) atomicAdd(&sc->hist[(int)((v >> shift) & 255u)], 1);
     }
     __syncthreads();
@@ -128,15 +141,17 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
     __syncthreads();
     const int d = sc->sel_digit, above = sc->sel_above, cnt = sc->sel_cnt;
     __syncthreads();
-    prefix |= (uint64_t)d << shift;
+    prefix = (prefix & ~(0xFFull << shift)) | ((uint64_t)d << shift);
     pmask |= 0xFFull << shift;
     kk -= above;
-    if (cnt == kk) break;   // the whole bucket is inside the top-k
+    if (cnt == kk || shift == 0) break;   // whole bucket inside the top-k, or the key is resolved
+    shift = shift - 8 > 0 ? shift - 8 : 0;
   }
   return prefix;
 }
 
 // In-place, order-preserving compaction of buf[0..n) to the keys >= T. Returns the new count.
+// Two barriers per NT-key chunk; warp 0 scans the per-warp counts.
 template <int NT>
 __device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -144,20 +159,176 @@ __device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc
   int running = 0;
   for (int base = 0; base < n; base += NT) {
     const int i = base + tid;
-    uint64_t v = (i < n) ? buf[i] : 0ull;
+    const uint64_t v = (i < n) ? buf[i] : 0ull;
     const bool keep = (i < n) && v >= T;
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) sc->warp_cnt[warp] = __popc(bal);
     __syncthreads();   // all reads of this chunk done, warp counts visible
-    int off = running;
-    for (int w = 0; w < warp; ++w) off += sc->warp_cnt[w];
-    int tot = running;
-    for (int w = 0; w < NW; ++w) tot += sc->warp_cnt[w];
-    if (keep) buf[off + __popc(bal & lanemask_lt())] = v;
+    if (warp == 0) {
+      const int c = lane < NW ? sc->warp_cnt[lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      if (lane < NW) sc->hist[lane] = incl - c;   // exclusive warp offsets
+      if (lane == 31) sc->total = incl;
+    }
     __syncthreads();
-    running = tot;
+    if (keep) buf[running + sc->hist[warp] + __popc(bal & lanemask_lt())] = v;
+    running += sc->total;
   }
+  __syncthreads();
   return running;
+}
+
+// Bitonic compare-exchange of element i against its partner value pv for stage (k, j):
+// descending overall; the lower index of a pair keeps the max inside descending blocks.
+LINR_DEV uint64_t bitonic_pick(uint64_t v, uint64_t pv, int i, int k, int j) {
+  const bool desc = (i & k) == 0;
+  const bool lower = (i & j) == 0;
+  const bool take_max = (lower == desc);
+  return take_max ? (v > pv ? v : pv) : (v < pv ? v : pv);
+}
+
+LINR_DEV uint64_t shfl_xor_u64(uint64_t v, int m) {
+  const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+  const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+LINR_DEV uint64_t shfl_idx_u64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+LINR_DEV uint64_t shfl_up_u64(uint64_t v, int d) {
+  const uint32_t lo = __shfl_up_sync(0xffffffffu, (uint32_t)v, d);
+  const uint32_t hi = __shfl_up_sync(0xffffffffu, (uint32_t)(v >> 32), d);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// MSD bucket sort, descending: keys s[0..n) (n <= 2048) -> out[0..n). Buckets = 11 bits below the
+// highest bit where the keys differ (2048 buckets, scatter by atomic cursors); buckets of <= 8
+// keys are insertion-sorted by one thread, buckets of <= 64 keys by one warp in registers
+// (bitonic over shuffles). Returns false (out undefined) if a bucket holds more than 64 keys;
+// the caller then sorts with the general bitonic network.
+struct BucketScratch {
+  int hist[2048];
+  int wtot[32];
+  int maxb;
+  int nbig;
+  int big[1024];
+  unsigned long long red_and, red_or;
+};
+template <int NT>
+__device__ bool block_bucket_sort_desc(const uint64_t* s, int n, uint64_t* out, BucketScratch* sc) {
+  constexpr int NW = NT / 32;
+  constexpr int BPW = 2048 / NW;
+  constexpr int BPL = BPW / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long a = ~0ull, o = 0ull;
+  for (int i = tid; i < n; i += NT) {
+    const uint64_t v = s[i];
+    a &= v;
+    o |= v;
+  }
+  for (int off = 16; off; off >>= 1) {
+    a &= __shfl_xor_sync(0xffffffffu, a, off);
+    o |= __shfl_xor_sync(0xffffffffu, o, off);
+  }
+  if (tid == 0) { sc->red_and = ~0ull; sc->red_or = 0ull; sc->maxb = 0; sc->nbig = 0; }
+  for (int i = tid; i < 2048; i += NT) sc->hist[i] = 0;
+  __syncthreads();
+  if (lane == 0) { atomicAnd(&sc->red_and, a); atomicOr(&sc->red_or, o); }
+  __syncthreads();
+  const unsigned long long diff = sc->red_and ^ sc->red_or;
+  const int hb = diff ? 63 - __clzll((long long)diff) : 0;
+  const int shift = hb - 10 > 0 ? hb - 10 : 0;
+  for (int i = tid; i < n; i += NT) atomicAdd(&sc->hist[(int)((s[i] >> shift) & 2047u)], 1);
+  __syncthreads();
+  // exclusive offsets in descending digit order, stored back into hist as scatter cursors
+  int c[BPL], sum = 0;
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    c[i] = sc->hist[2047 - warp * BPW - lane * BPL - i];
+    sum += c[i];
+  }
+  int incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) sc->wtot[warp] = incl;
+  __syncthreads();
+  int acc = incl - sum, mx = 0;
+  for (int w = 0; w < warp; ++w) acc += sc->wtot[w];
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    sc->hist[2047 - warp * BPW - lane * BPL - i] = acc;
+    acc += c[i];
+    mx = c[i] > mx ? c[i] : mx;
+  }
+  for (int off = 16; off; off >>= 1) {
+    const int t = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = t > mx ? t : mx;
+  }
+  if (lane == 0) atomicMax(&sc->maxb, mx);
+  __syncthreads();
+  if (sc->maxb > 64) return false;
+  for (int i = tid; i < n; i += NT) {
+    const uint64_t v = s[i];
+    out[atomicAdd(&sc->hist[(int)((v >> shift) & 2047u)], 1)] = v;
+  }
+  __syncthreads();
+  // bucket d spans [end(d+1), end(d)) where end = the advanced cursor
+  for (int d = tid; d < 2048; d += NT) {
+    const int end = sc->hist[d];
+    const int start = (d == 2047) ? 0 : sc->hist[d + 1];
+    if (end - start > 8) {
+      sc->big[atomicAdd(&sc->nbig, 1)] = d;
+      continue;
+    }
+    for (int i = start + 1; i < end; ++i) {
+      const uint64_t x = out[i];
+      int j = i - 1;
+      while (j >= start && out[j] < x) {
+        out[j + 1] = out[j];
+        --j;
+      }
+      out[j + 1] = x;
+    }
+  }
+  __syncthreads();
+  for (int bi = warp; bi < sc->nbig; bi += NW) {   // warp per medium bucket (<= 64 keys)
+    const int d = sc->big[bi];
+    const int end = sc->hist[d];
+    const int start = (d == 2047) ? 0 : sc->hist[d + 1];
+    const int m = end - start;
+    uint64_t x0 = lane < m ? out[start + lane] : 0ull;
+    uint64_t x1 = lane + 32 < m ? out[start + lane + 32] : 0ull;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j == 32) {
+          const uint64_t mxv = x0 > x1 ? x0 : x1, mnv = x0 > x1 ? x1 : x0;
+          x0 = mxv;
+          x1 = mnv;
+        } else {
+          const uint64_t p0 = shfl_xor_u64(x0, j), p1 = shfl_xor_u64(x1, j);
+          x0 = bitonic_pick(x0, p0, lane, k, j);
+          x1 = bitonic_pick(x1, p1, lane + 32, k, j);
+        }
+      }
+    }
+    if (lane < m) out[start + lane] = x0;
+    if (lane + 32 < m) out[start + lane + 32] = x1;
+  }
+  __syncthreads();
+  return true;
 }
 
 // Bitonic sort, descending, of s[0..P2) (P2 a power of two). All threads call.
@@ -176,6 +347,88 @@ __device__ void block_sort_desc(uint64_t* s, int P2) {
       __syncthreads();
     }
   }
+}
+
+// One warp sorts s[0..64) descending in registers (2 elements per lane: i = lane, lane + 32).
+LINR_DEV void warp_sort64_desc(uint64_t* s) {
+  const int lane = threadIdx.x & 31;
+  uint64_t a = s[lane], b = s[lane + 32];
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        const uint64_t mx = a > b ? a : b, mn = a > b ? b : a;
+        a = mx;   // i = lane < 32 is the lower index and k = 64 is a descending block
+        b = mn;
+      } else {
+        const uint64_t pa = shfl_xor_u64(a, j), pb = shfl_xor_u64(b, j);
+        a = bitonic_pick(a, pa, lane, k, j);
+        b = bitonic_pick(b, pb, lane + 32, k, j);
+      }
+    }
+  }
+  __syncwarp();
+  s[lane] = a;
+  s[lane + 32] = b;
+  __syncwarp();
+}
+
+// CTA-wide bitonic sort (descending) of s[0..P2), 64 <= P2 <= 4*NT, P2 a power of two. Elements
+// live in registers (element i at thread i % NT, slot i / NT); partners inside a warp are
+// exchanged by shuffles, across warps through the double-buffered scratch (2*P2 keys), across
+// slots in registers. Far fewer barriers than a shared-memory-only network.
+template <int NT>
+__device__ void block_sort_desc_reg(uint64_t* s, int P2, uint64_t* scratch) {
+  constexpr int EMAX = 4;
+  const int t = threadIdx.x;
+  const int E = P2 > NT ? P2 / NT : 1;
+  uint64_t v[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) v[e] = (e < E && t + e * NT < P2) ? s[t + e * NT] : 0ull;
+  int buf = 0;
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= NT) {   // partner in another slot of the same thread
+        const int ej = j / NT;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e >= E || (e & ej)) continue;   // handle each pair once, from its lower slot
+          const int i = t + e * NT;
+          const uint64_t a = v[e], b = v[e + ej];
+          const bool desc = (i & k) == 0;
+          const uint64_t mx = a > b ? a : b, mn = a > b ? b : a;
+          v[e] = desc ? mx : mn;
+          v[e + ej] = desc ? mn : mx;
+        }
+      } else if (j >= 32) {
+        uint64_t* x = scratch + buf * P2;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e)
+          if (e < E && t + e * NT < P2) x[t + e * NT] = v[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          const int i = t + e * NT;
+          if (e < E && i < P2) v[e] = bitonic_pick(v[e], x[i ^ j], i, k, j);
+        }
+        buf ^= 1;
+      } else {
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e < E) {   // E is uniform: every lane of the warp shuffles
+            const uint64_t pv = shfl_xor_u64(v[e], j);
+            v[e] = bitonic_pick(v[e], pv, t + e * NT, k, j);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e)
+    if (e < E && t + e * NT < P2) s[t + e * NT] = v[e];
+  __syncthreads();
 }
 
 __host__ __device__ inline int next_pow2(int x) {

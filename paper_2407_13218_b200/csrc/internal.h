@@ -14,12 +14,37 @@ struct DevHeader {               // lives in device memory
   unsigned long long hwm;        // local rows [0, hwm) may be live
   unsigned long long skipped;    // out-of-shard ids seen by update/delete
   unsigned long long overflow;   // scan buffer overflows (must stay 0; checked by tests)
+  unsigned int done_ctas;        // scan CTAs finished (fused merge ticket; self-resetting)
+  unsigned int merged;           // users merged by the fused tail (self-resetting)
 };
 
 struct KClause {                 // clause as the kernels see it (16 B)
   unsigned long long mask;
   uint32_t word;
   uint32_t rev;
+};
+
+// Merge L partition results per user into the final top-K. Partition l of user u provides a
+// sorted descending sample samp[l][u][0..ms) (its top-ms keys, 0-padded) and a list of all its
+// candidate keys list[l][u][0..cnt) in any order (the sample keys included).
+struct MergeParams {
+  const uint64_t* samp;
+  int64_t samp_sl, samp_su;      // strides (keys) per partition / per user
+  int ms;                        // sample length (<= 64)
+  const uint64_t* list;
+  int64_t list_sl, list_su;
+  const int* cnt;                // cnt[l*cnt_sl + u*cnt_su]; null: every list has list_len keys (0-padded)
+  int64_t cnt_sl, cnt_su;
+  int list_len;                  // max keys per list
+  const int64_t* pass;           // pass[l*pstride_l + u*pstride_u]
+  int64_t pstride_l, pstride_u;
+  int L, K;
+  int64_t* out_ids;              // [B][K] (mode 0)
+  float* out_scores;             // [B][K] (mode 0)
+  uint64_t* out_keys;            // [B][K] (mode 1)
+  int64_t* out_pass;             // [B] (may be null)
+  int mode;                      // 0: decode ids/scores, 1: sorted keys
+  unsigned long long* dbg;       // diagnostics timers
 };
 
 // Parameters of one GEMV scan launch (passed by value; <= 4 KB).
@@ -35,10 +60,16 @@ struct ScanParams {
   int K;
   int C;                         // soft capacity of the per-user CTA buffer
   int bufcap;                    // hard capacity (C + headroom)
+  int list_cap;                  // capacity of each per-CTA output list (keys)
   uint32_t wmask;                // attribute words referenced by any clause
   const void* q;                 // [nu][V][dim] queries of this launch's users
-  uint64_t* out_keys;            // [nu][gridDim.x][K]
+  uint64_t* out_samp;            // [nu][gridDim.x][32] sorted top-32 of each CTA
+  uint64_t* out_list;            // [nu][gridDim.x][list_cap] every key the CTA kept (unsorted)
+  int* out_cnt;                  // [nu][gridDim.x] keys in out_list
   int64_t* out_pass;             // [nu][gridDim.x]
+  unsigned long long* dbg;        // diagnostics timers (null unless linr_debug_timers(1))
+  int fuse_merge;                // 1: the last nu CTAs run the merge (mp) for this launch's users
+  MergeParams mp;                // merge of this launch's users (user index relative to the launch)
   int ncl[8];
   KClause cl[8][16];
 };
@@ -46,7 +77,9 @@ struct ScanParams {
 struct ScanCfg {                 // launch geometry chosen for one (dtype, dim, nqv)
   int nt;                        // threads per CTA
   int rows_per_iter;             // rows a warp scores per inner iteration (append burst bound)
+  int ring_bytes;                // per-warp cp.async row ring (stages x rows_per_iter x row bytes)
 };
+constexpr int kScanSample = 32;  // sorted per-CTA sample length
 
 // Launch the fused filter + score + CTA top-K scan. nqv = padded vectors per launch (1,2,4,8).
 cudaError_t launch_scan_gemv(int dtype, int dim, int nqv, const ScanParams& p, int grid,
@@ -54,21 +87,8 @@ cudaError_t launch_scan_gemv(int dtype, int dim, int nqv, const ScanParams& p, i
 bool scan_gemv_supported(int dtype, int dim, int nqv);
 ScanCfg scan_gemv_cfg(int dtype, int dim, int nqv);
 
-// Merge L sorted key lists per user into the final top-K.
-struct MergeParams {
-  const uint64_t* keys;          // list l of user u at keys + l*stride_l + u*stride_u, length K
-  int64_t stride_l, stride_u;
-  const int64_t* pass;           // pass[l*pstride_l + u*pstride_u]
-  int64_t pstride_l, pstride_u;
-  int L, K, m;                   // m: per-list sample size for the pruned path
-  int64_t* out_ids;              // [B][K] (mode 0)
-  float* out_scores;             // [B][K] (mode 0)
-  uint64_t* out_keys;            // [B][K] (mode 1)
-  int64_t* out_pass;             // [B] (may be null)
-  int mode;                      // 0: decode ids/scores, 1: keys
-};
 cudaError_t launch_merge(const MergeParams& p, int B, cudaStream_t st);
-int merge_sample_size(int L, int K);
+size_t merge_smem();
 
 // index maintenance kernels
 cudaError_t launch_attr_soa(const uint64_t* src, int64_t n, int W, uint64_t* dst_soa, int64_t cap_pad,
@@ -85,5 +105,6 @@ cudaError_t launch_generate(int dtype, int dim, int W, uint64_t seed, int mode, 
                             bool attrs_soa, cudaStream_t st);
 
 void set_error(const std::string& msg);
+unsigned long long* debug_buffer();
 
 }  // namespace linr

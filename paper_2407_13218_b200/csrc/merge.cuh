@@ -1,0 +1,211 @@
+// Merge of L partition results into the final top-K of one user (CTA-wide device function).
+//
+// Used twice on the hot path: (a) at the end of the scan, L = number of scan CTAs (partition =
+// one CTA's item range; run by the last CTAs of the scan kernel itself, or by merge_kernel);
+// (b) after the cross-GPU all-gather, L = number of shards (BASELINE.json north_star: "an NCCL
+// allgather of K (score, id) pairs ... feeds a final merge"). Exact by reading R13: the union of
+// the partitions' top-Ks contains the global top-K under the total key order (score desc, id asc).
+//
+// Each partition provides a sorted sample (its top ms keys) and a list of all its candidate keys.
+// LB = K-th largest key of the union of the samples is a lower bound of the answer's K-th key
+// (those K keys exist), so the answer is {samples >= LB} plus, only for partitions whose whole
+// sample is >= LB ("saturated"), their list keys in [LB, sample[ms-1]). For item ranges of
+// similar statistics saturation is rare and the merge touches only the samples. If the samples
+// hold fewer than K keys, every list key is gathered (exact fallback, in global memory if large).
+#pragma once
+#include "common.cuh"
+#include "internal.h"
+
+namespace linr {
+
+constexpr int kMergeCap = 16384;    // keys staged in shared memory (128 KB)
+constexpr int kMergeOut = 4096;     // survivor / sort buffer (32 KB)
+constexpr int kMergeRegs = 16;      // sample keys held per thread on the fast path
+
+struct MergeCtl {
+  SelScratch sel;
+  BucketScratch bs;
+  int cnt;
+  int nnz;
+  long long pass;
+};
+
+constexpr size_t merge_smem_bytes() {
+  return ((sizeof(MergeCtl) + 15) & ~size_t(15)) + (size_t)(kMergeCap + kMergeOut) * 8;
+}
+
+// Append the nonzero keys >= lb among n_items keys get(i) to dst (warp-aggregated); returns the count.
+template <int NT, typename Get>
+__device__ int merge_gather(uint64_t* dst, int cap, MergeCtl* ctl, int n_items, Get get, uint64_t lb) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) ctl->cnt = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n_items; i0 += NT) {   // uniform trip count: full-warp ballots
+    const int i = i0 + tid;
+    uint64_t v = 0ull;
+    if (i < n_items) v = get(i);
+    const bool keep = v != 0ull && v >= lb;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (bal) {
+      const int leader = __ffs(bal) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(&ctl->cnt, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      const int pos = base + __popc(bal & lanemask_lt());
+      if (keep && pos < cap) dst[pos] = v;
+    }
+  }
+  __syncthreads();
+  return ctl->cnt;
+}
+
+// Warp-aggregated append of v (if keep) at ctl->cnt.
+LINR_DEV void merge_append(uint64_t* dst, int cap, MergeCtl* ctl, bool keep, uint64_t v) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+  if (bal) {
+    const int leader = __ffs(bal) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&ctl->cnt, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int pos = base + __popc(bal & lanemask_lt());
+    if (keep && pos < cap) dst[pos] = v;
+  }
+}
+
+template <int NT>
+__device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
+  MergeCtl* ctl = reinterpret_cast<MergeCtl*>(smem);
+  uint64_t* s = reinterpret_cast<uint64_t*>(smem + ((sizeof(MergeCtl) + 15) & ~size_t(15)));
+  uint64_t* s2 = s + kMergeCap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int L = p.L, K = p.K, ms = p.ms;
+  const uint64_t* samp = p.samp + (int64_t)u * p.samp_su;
+  const uint64_t* list = p.list + (int64_t)u * p.list_su;
+  const int64_t ssl = p.samp_sl, lsl = p.list_sl, csl = p.cnt_sl;
+  const int* cntp = p.cnt ? p.cnt + (int64_t)u * p.cnt_su : nullptr;
+  const int len = p.list_len;
+  const int DB = 4096 + u * 8;
+  dbg_mark(p.dbg, DB + 0);
+
+  if (tid == 0) { ctl->nnz = 0; ctl->cnt = 0; }
+  if (warp == 0) {
+    long long acc = 0;
+    for (int l = lane; l < L; l += 32) acc += p.pass[(int64_t)l * p.pstride_l + (int64_t)u * p.pstride_u];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ctl->pass = acc;
+  }
+  auto lcount = [cntp, csl, len](int l) -> int { return cntp ? cntp[(int64_t)l * csl] : len; };
+  __syncthreads();
+
+  int n = -1;
+  const int ns = L * ms;
+  if (ns <= kMergeRegs * NT && ns <= kMergeCap) {
+    // 1. samples: batched loads into registers (all in flight at once), copy to shared memory
+    uint64_t r[kMergeRegs];
+#pragma unroll
+    for (int e = 0; e < kMergeRegs; ++e) {
+      const int i = tid + e * NT;
+      r[e] = 0ull;
+      if (i < ns) {
+        const int l = i / ms;
+        r[e] = samp[(int64_t)l * ssl + (i - l * ms)];
+      }
+    }
+    int nz = 0;
+#pragma unroll
+    for (int e = 0; e < kMergeRegs; ++e) {
+      const int i = tid + e * NT;
+      if (i < ns) {
+        s[i] = r[e];
+        nz += r[e] != 0ull;
+      }
+    }
+    for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    if (lane == 0 && nz) atomicAdd(&ctl->nnz, nz);
+    __syncthreads();
+    dbg_mark(p.dbg, DB + 1);
+    if (ctl->nnz >= K) {
+      // 2. LB = K-th largest sample key (zero padding sorts below it)
+      const uint64_t lb = block_select_ge<NT>([s](int i) { return s[i]; }, ns, K, &ctl->sel);
+      dbg_mark(p.dbg, DB + 2);
+      // 3. survivors: sample keys >= lb (exactly K) + saturated partitions' keys in [lb, last)
+#pragma unroll
+      for (int e = 0; e < kMergeRegs; ++e) merge_append(s2, kMergeOut, ctl, r[e] != 0ull && r[e] >= lb, r[e]);
+      for (int l = warp; l < L; l += NW) {
+        const uint64_t last = s[l * ms + ms - 1];   // the sample is staged in shared memory
+        if (last < lb) continue;   // warp-uniform
+        const int c = lcount(l);
+        const uint64_t* lp = list + (int64_t)l * lsl;
+        for (int j0 = 0; j0 < c; j0 += 32) {
+          const int j = j0 + lane;
+          const uint64_t v = j < c ? lp[j] : 0ull;
+          merge_append(s2, kMergeOut, ctl, v != 0ull && v >= lb && v < last, v);
+        }
+      }
+      __syncthreads();
+      n = ctl->cnt;
+      if (n > kMergeOut) n = -1;
+    }
+  }
+  dbg_mark(p.dbg, DB + 3);
+  if (n < 0) {
+    // exact fallback: every list key (a partition's list includes its sample keys)
+    const int items = L * len;
+    auto get = [list, lsl, len, lcount](int i) -> uint64_t {
+      const int l = i / len, j = i - l * len;
+      return j < lcount(l) ? list[(int64_t)l * lsl + j] : 0ull;
+    };
+    int n1 = merge_gather<NT>(s, kMergeCap, ctl, items, get, 1ull);
+    if (n1 > kMergeCap) {
+      // zeros sort below every real key and K <= n1, so they are never selected
+      const uint64_t T = block_select_ge<NT>(get, items, K, &ctl->sel);
+      n1 = merge_gather<NT>(s, kMergeCap, ctl, items, get, T);
+    }
+    if (n1 > K) {
+      const uint64_t T = block_select_ge<NT>([s](int i) { return s[i]; }, n1, K, &ctl->sel);
+      n1 = block_compact_ge<NT>(s, n1, T, &ctl->sel);
+    }
+    for (int i = tid; i < n1; i += NT) s2[i] = s[i];
+    __syncthreads();
+    n = n1;
+  } else if (n > K) {
+    const uint64_t T = block_select_ge<NT>([s2](int i) { return s2[i]; }, n, K, &ctl->sel);
+    n = block_compact_ge<NT>(s2, n, T, &ctl->sel);
+  }
+  dbg_mark(p.dbg, DB + 4);
+  // 4. sort the <= K survivors: bucket sort, general bitonic if a bucket is too full
+  const uint64_t* sorted = s;
+  const bool bucket_ok = block_bucket_sort_desc<NT>(s2, n, s, &ctl->bs);
+  if (p.dbg != nullptr && tid == 0) p.dbg[6144 + u * 4 + 0] = (unsigned long long)ctl->bs.maxb | ((unsigned long long)bucket_ok << 32);
+  if (!bucket_ok) {
+    const int P2 = next_pow2(n > 1 ? n : 1);
+    for (int i = n + tid; i < P2; i += NT) s2[i] = 0ull;
+    __syncthreads();
+    block_sort_desc<NT>(s2, P2);
+    sorted = s2;
+  }
+  dbg_mark(p.dbg, DB + 5);
+
+  if (p.mode == 0) {
+    for (int j = tid; j < K; j += NT) {
+      const int64_t at = (int64_t)u * K + j;
+      if (j < n) {
+        p.out_ids[at] = key_id(sorted[j]);
+        p.out_scores[at] = key_score(sorted[j]);
+      } else {
+        p.out_ids[at] = -1;
+        p.out_scores[at] = -INFINITY;
+      }
+    }
+  } else {
+    for (int j = tid; j < K; j += NT) p.out_keys[(int64_t)u * K + j] = (j < n) ? sorted[j] : 0ull;
+  }
+  if (tid == 0 && p.out_pass) p.out_pass[u] = ctl->pass;
+  dbg_mark(p.dbg, DB + 6);
+  if (p.dbg != nullptr && tid == 0) p.dbg[DB + 7] = (unsigned long long)n;
+  __syncthreads();
+}
+
+}  // namespace linr

@@ -4,20 +4,24 @@
 // without materialising a slice) and never reach top-K (reading R1: exclusion, not zero-masking).
 // The fully fused filter+score+top-K kernel is the option §6 describes for regular KNN.
 //
-// Per warp tile of 256 items (8 per lane):
-//   1. liveness bits (1 bit/item) + attribute words (8 B/item, coalesced 256 B per warp load);
-//      evaluate every user's clauses -> per-(user,item) pass bits; compact passing items into a
-//      per-warp list in shared memory (ballot + popc).
-//   2. stream only the passing rows: LPR lanes per row, one 16-byte ld.global.nc per lane per
-//      chunk, R rows in flight per lane group; fp32 FFMA (f32/f16/bf16) or exact int32 DP4A (int8)
-//      against the query chunk held in registers; butterfly-reduce over the LPR lanes; max over the
-//      user's V vectors (reading R12).
+// One persistent CTA per SM owns a contiguous range of 256-item tiles; its warps take tiles
+// dynamically. Per warp tile (8 items per lane):
+//   1. liveness bits (1 bit/item) + attribute words (8 B/item, coalesced 256 B per warp load,
+//      prefetched one tile ahead in registers); evaluate every user's clauses -> per-(user,item)
+//      pass bits; compact passing items into a per-warp list in shared memory (ballot + popc).
+//   2. gather only the passing rows with cp.async (LDGSTS, 16 B per lane, no register cost) into a
+//      per-warp shared-memory ring of S stages, so S-1 row groups are in flight while one is
+//      scored; LPR lanes per row, each owning CPL chunks; fp32 FFMA (f32/f16/bf16) or exact int32
+//      DP4A (int8) against the query chunk held in registers; butterfly-reduce over the LPR lanes;
+//      max over the user's V vectors (reading R12).
 //   3. threshold test against the CTA's current per-user bound, warp-aggregated append of packed
-//      (score,id) keys to the CTA's shared-memory buffer; when a buffer passes its soft capacity the
-//      whole CTA radix-selects the K-th key and compacts (exact: keys below the K-th of K kept keys
-//      can never enter the top-K).
-//   4. at the end each CTA sorts its <= K survivors and writes them; the merge kernel combines the
-//      per-CTA lists.
+//      (score,id) keys to the CTA's shared-memory buffer, and insertion into the warp's sorted
+//      top-32 register list (warp select). When a buffer passes its soft capacity the whole CTA
+//      radix-selects the K-th key and compacts (exact: keys below the K-th of K kept keys can
+//      never enter the top-K).
+//   4. at the end the CTA merges its warps' top-32 lists into its sorted top-32 "sample" and
+//      writes the sample plus its (unsorted) buffer; merge.cu combines the CTAs: the K-th key of
+//      the union of samples bounds the answer from below, so normally only samples are read.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -26,21 +30,43 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "merge.cuh"
 
 namespace linr {
 
-template <int DT, int D>
+// Row geometry. LPR lanes cooperate on one row, each owning CPL 16-byte chunks (chunk gl + c*LPR,
+// so one load instruction of a row group reads LPR*16 contiguous bytes: full 32-byte sectors);
+// RPW rows per warp instruction, R rows in flight per lane group. LPR = 4 keeps the per-row
+// bookkeeping (butterfly reduce, key, threshold, append ballot) amortised over 8 rows per warp
+// instruction while keeping 64-byte contiguous segments per row per load.
+// Row geometry. LPR lanes cooperate on one row, each owning CPL 16-byte chunks (chunk gl + c*LPR,
+// so one load instruction of a row group reads LPR*16 contiguous bytes: full 32-byte sectors);
+// RPW rows per warp instruction, R rows in flight per lane group. Few lanes per row (LPR = 4)
+// amortise the per-row bookkeeping (butterfly reduce, key, threshold, append ballot) over 8 rows
+// per warp instruction; with more query vectors LPR grows so the per-lane query chunks (NQV*CPL
+// chunks held in registers) stay within budget.
+constexpr int geom_lpr(int CH, int NQV, int PER) {
+  int lpr = CH / 4 > 4 ? CH / 4 : 4;
+  if (lpr > 32) lpr = 32;
+  if (lpr > CH) lpr = CH;
+  while (lpr < CH && lpr < 32 && NQV * (CH / lpr) * PER > 32) lpr *= 2;
+  return lpr;
+}
+
+template <int DT, int D, int NQV = 1>
 struct RowGeom {
   static constexpr int ESZ = (DT == LINR_F32) ? 4 : (DT == LINR_I8 ? 1 : 2);
   static constexpr int ROWB = D * ESZ;          // bytes per row
   static constexpr int CH = ROWB / 16;          // 16-byte chunks per row
-  static constexpr int LPR = CH < 32 ? CH : 32; // lanes per row
+  static constexpr int EPC = 16 / ESZ;          // elements per chunk
+  static constexpr int PER = (DT == LINR_I8) ? 4 : EPC;   // query registers per chunk
+  static constexpr int LPR = geom_lpr(CH, NQV, PER);      // lanes per row
   static constexpr int CPL = CH / LPR;          // chunks per lane
   static constexpr int RPW = 32 / LPR;          // rows per warp step
   static constexpr int R = CPL >= 4 ? 1 : 4 / CPL;  // rows in flight per lane group
   static constexpr int RPI = RPW * R;           // rows per warp iteration
-  static constexpr int EPC = 16 / ESZ;          // elements per chunk
   static_assert(ROWB % 16 == 0, "row must be a multiple of 16 bytes");
+  static_assert(CH % LPR == 0, "chunks must split evenly over the lanes of a row");
 };
 
 template <int DT>
@@ -111,9 +137,15 @@ struct ScanCtl {
   int flag;                            // a buffer reached its soft capacity
   int done;                            // warps finished with their tiles
   int overflow;                        // appends beyond the hard capacity (must stay 0)
+  int next_tile;                       // CTA-local dynamic tile counter
+  int wcnt;                            // write counter for the final list
+  int ticket;                          // fused-merge ticket of this CTA
 };
 
 static_assert(sizeof(ScanCtl) + 16 <= 2048, "host plan reserves 2 KB for ScanCtl (api.cu kScanCtlBytes)");
+
+constexpr int kStages = 4;        // cp.async row-ring depth per warp
+constexpr int kSample = kScanSample;   // sorted per-CTA sample length (merge pruning)
 
 LINR_DEV bool scan_flag(const ScanCtl* ctl, int lane) {
   int f = 0;
@@ -121,9 +153,38 @@ LINR_DEV bool scan_flag(const ScanCtl* ctl, int lane) {
   return __shfl_sync(0xffffffffu, f, 0) != 0;
 }
 
+LINR_DEV void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+LINR_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+LINR_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Insert `k` (> the current 32nd) into a descending 32-list spread over the warp (lane i = rank i).
+LINR_DEV uint64_t wlist_insert(uint64_t wl, uint64_t k, int lane) {
+  const uint64_t up = shfl_up_u64(wl, 1);
+  if (wl > k) return wl;
+  return (lane == 0 || up > k) ? k : up;
+}
+
+// Top-32 of two descending 32-lists a (this lane: a_i) and b (this lane: b_i), descending.
+LINR_DEV uint64_t wlist_merge(uint64_t a, uint64_t b, int lane) {
+  const uint64_t br = shfl_idx_u64(b, 31 - lane);
+  uint64_t c = a > br ? a : br;   // bitonic, holds the top-32 of a U b
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint64_t pc = shfl_xor_u64(c, j);
+    const bool lower = (lane & j) == 0;
+    c = lower ? (c > pc ? c : pc) : (c < pc ? c : pc);
+  }
+  return c;
+}
+
 template <int NT>
 __device__ __noinline__ void scan_compact_all(ScanCtl* ctl, uint64_t* bufs, const ScanParams& p) {
   __syncthreads();   // every warp of the CTA is here (flag checks are warp-uniform)
+  if (p.dbg != nullptr && threadIdx.x == 0) atomicAdd(&p.dbg[blockIdx.x * 8 + 7], 1ull);
   for (int u = 0; u < p.nu; ++u) {
     const int n = min(ctl->count[u], p.bufcap);
     if (n > p.K) {
@@ -143,24 +204,28 @@ __device__ __noinline__ void scan_compact_all(ScanCtl* ctl, uint64_t* bufs, cons
 
 template <int DT, int D, int NQV, int NT>
 __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant__ ScanParams p) {
-  using G = RowGeom<DT, D>;
+  using G = RowGeom<DT, D, NQV>;
   constexpr bool kInt = (DT == LINR_I8);
   using acc_t = typename std::conditional<kInt, int, float>::type;
   constexpr int NW = NT / 32;
   constexpr int NU = NQV;   // at most one user per vector
+  constexpr int STAGE = G::RPI * G::ROWB;   // bytes of one ring stage
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScanCtl* ctl = reinterpret_cast<ScanCtl*>(smem_raw);
   uint64_t* bufs = reinterpret_cast<uint64_t*>(smem_raw + ((sizeof(ScanCtl) + 15) & ~size_t(15)));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint16_t* wlist = reinterpret_cast<uint16_t*>(bufs + (size_t)p.nu * p.bufcap) + warp * kTileItems;
+  uint16_t* wlist_all = reinterpret_cast<uint16_t*>(bufs + (size_t)p.nu * p.bufcap);
+  uint16_t* wlist = wlist_all + warp * kTileItems;
+  unsigned char* rings = reinterpret_cast<unsigned char*>(wlist_all + NW * kTileItems);   // 16B aligned
+  unsigned char* ring = rings + (size_t)warp * kStages * STAGE;
 
   if (tid < kMaxUsers) {
     ctl->thr[tid] = 0ull;
     ctl->count[tid] = 0;
     ctl->pass[tid] = 0u;
   }
-  if (tid == 0) { ctl->flag = 0; ctl->done = 0; ctl->overflow = 0; }
+  if (tid == 0) { ctl->flag = 0; ctl->done = 0; ctl->overflow = 0; ctl->next_tile = 0; }
 
   // ---- query chunks into registers (lane group member gl owns chunks gl + c*LPR)
   const int g = lane / G::LPR, gl = lane % G::LPR;
@@ -187,19 +252,47 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     }
   }
   __syncthreads();
+  dbg_mark(p.dbg, blockIdx.x * 8 + 0);
 
+  // ---- this CTA's contiguous tile range; warps take tiles from it dynamically
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
   const int64_t ntiles = (hwm + kTileItems - 1) / kTileItems;
-  uint32_t pcnt[NU];
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  auto grab = [&]() -> int64_t {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->next_tile, 1);
+    return t_begin + __shfl_sync(0xffffffffu, t, 0);
+  };
+  const bool w0 = (p.wmask & 1u) != 0;
+  auto prefetch = [&](int64_t tile, uint64_t (&a)[8], uint32_t& lw) {
+    const int64_t base = tile * kTileItems;
+    lw = (lane < 8) ? __ldg(p.live + (base >> 5) + lane) : 0u;
+    if (w0) {
+      const uint64_t* ap = p.attr + base + lane;
 #pragma unroll
-  for (int u = 0; u < NU; ++u) pcnt[u] = 0;
+      for (int t = 0; t < 8; ++t) a[t] = ldg_stream_u64(ap + t * 32);
+    }
+  };
 
-  for (int64_t tile = (int64_t)blockIdx.x * NW + warp; tile < ntiles; tile += (int64_t)gridDim.x * NW) {
+  uint32_t pcnt[NU];
+  uint64_t wtop[NU];   // this warp's sorted top-32 per user (lane i = rank i)
+#pragma unroll
+  for (int u = 0; u < NU; ++u) { pcnt[u] = 0; wtop[u] = 0ull; }
+
+  int64_t tile = grab();
+  uint64_t a[8];
+  uint32_t lw = 0;
+  if (tile < t_end) prefetch(tile, a, lw);
+  while (tile < t_end) {
     if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
+    const int64_t next = grab();
+    uint64_t na[8];
+    uint32_t nlw = 0;
+    if (next < t_end) prefetch(next, na, nlw);
     const int64_t base = tile * kTileItems;
 
     // ---- 1. liveness + clauses -> pass bits
-    const uint32_t lw = (lane < 8) ? __ldg(p.live + (base >> 5) + lane) : 0u;
     uint32_t mylive = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) mylive |= ((__shfl_sync(0xffffffffu, lw, t) >> lane) & 1u) << t;
@@ -210,10 +303,15 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
 #pragma unroll 1
       for (int w = 0; w < 4; ++w) {
         if (!((p.wmask >> w) & 1u)) continue;
-        uint64_t a[8];
-        const uint64_t* ap = p.attr + (size_t)w * p.cap_pad + base + lane;
+        uint64_t aw[8];
+        if (w == 0) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) a[t] = ldg_stream_u64(ap + t * 32);
+          for (int t = 0; t < 8; ++t) aw[t] = a[t];
+        } else {
+          const uint64_t* ap = p.attr + (size_t)w * p.cap_pad + base + lane;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) aw[t] = ldg_stream_u64(ap + t * 32);
+        }
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
           if (u >= p.nu) continue;
@@ -224,7 +322,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
             const bool rev = k.rev != 0;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
-              const bool hit = (a[t] & m) != 0ull;
+              const bool hit = (aw[t] & m) != 0ull;
               if (hit == rev) pb[u] &= ~(1u << t);
             }
           }
@@ -247,21 +345,39 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     for (int u = 0; u < NU; ++u) pcnt[u] += __popc(pb[u]);
     __syncwarp();
 
-    // ---- 2./3. stream passing rows, score, threshold, append
-    for (int j0 = 0; j0 < cnt; j0 += G::RPI) {
-      uint4 v[G::R][G::CPL];
-      uint32_t ent[G::R];
+    // ---- 2. gather passing rows through the cp.async ring
+    const int n_iter = (cnt + G::RPI - 1) / G::RPI;
+    auto issue = [&](int it) {
+      unsigned char* st = ring + (it % kStages) * STAGE;
 #pragma unroll
       for (int r = 0; r < G::R; ++r) {
-        const int idx = j0 + r * G::RPW + g;
-        ent[r] = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
-        const char* rowp = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (ent[r] >> 8)) * G::ROWB + gl * 16;
+        const int slot = r * G::RPW + g;
+        const int idx = it * G::RPI + slot;
+        const uint32_t e = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+        const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * G::ROWB + gl * 16;
 #pragma unroll
         for (int c = 0; c < G::CPL; ++c)
-          v[r][c] = ent[r] ? ldg_stream_v4(rowp + c * G::LPR * 16) : make_uint4(0, 0, 0, 0);
+          cp_async16(st + slot * G::ROWB + (gl + c * G::LPR) * 16, src + c * G::LPR * 16, e ? 16 : 0);
       }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int it = 0; it < kStages - 1; ++it) {
+      if (it < n_iter) issue(it); else cp_async_commit();
+    }
+    for (int it = 0; it < n_iter; ++it) {
+      if (it + kStages - 1 < n_iter) issue(it + kStages - 1); else cp_async_commit();
+      cp_async_wait<kStages - 1>();
+      const unsigned char* st = ring + (it % kStages) * STAGE;
 #pragma unroll
       for (int r = 0; r < G::R; ++r) {
+        const int slot = r * G::RPW + g;
+        const int idx = it * G::RPI + slot;
+        const uint32_t ent = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+        uint4 v[G::CPL];
+#pragma unroll
+        for (int c = 0; c < G::CPL; ++c)
+          v[c] = *reinterpret_cast<const uint4*>(st + slot * G::ROWB + (gl + c * G::LPR) * 16);
         acc_t s[NQV];
 #pragma unroll
         for (int j = 0; j < NQV; ++j) {
@@ -269,19 +385,19 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
 #pragma unroll
           for (int c = 0; c < G::CPL; ++c) {
             if constexpr (kInt) {
-              acc = __dp4a((int)v[r][c].x, (int)qi[j][c].x, acc);
-              acc = __dp4a((int)v[r][c].y, (int)qi[j][c].y, acc);
-              acc = __dp4a((int)v[r][c].z, (int)qi[j][c].z, acc);
-              acc = __dp4a((int)v[r][c].w, (int)qi[j][c].w, acc);
+              acc = __dp4a((int)v[c].x, (int)qi[j][c].x, acc);
+              acc = __dp4a((int)v[c].y, (int)qi[j][c].y, acc);
+              acc = __dp4a((int)v[c].z, (int)qi[j][c].z, acc);
+              acc = __dp4a((int)v[c].w, (int)qi[j][c].w, acc);
             } else {
-              acc = ChunkDot<DT>::dot(v[r][c], qf[j][c], acc);
+              acc = ChunkDot<DT>::dot(v[c], qf[j][c], acc);
             }
           }
 #pragma unroll
           for (int o = G::LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
           s[j] = acc;
         }
-        const uint32_t gid = p.row0 + (uint32_t)(base + (ent[r] >> 8));
+        const uint32_t gid = p.row0 + (uint32_t)(base + (ent >> 8));
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
           float su = -INFINITY;
@@ -290,7 +406,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
             if (uj[j] == u) su = fmaxf(su, (float)s[j]);
           bool cand = false;
           uint64_t key = 0ull;
-          if (u < p.nu && gl == 0 && ((ent[r] >> u) & 1u)) {
+          if (u < p.nu && gl == 0 && ((ent >> u) & 1u)) {
             key = make_key(su, gid);
             cand = key >= *(volatile const unsigned long long*)&ctl->thr[u];
           }
@@ -312,12 +428,26 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
               if (pos < p.bufcap) bufs[(size_t)u * p.bufcap + pos] = key;
               else atomicAdd(&ctl->overflow, 1);
             }
+            // warp select: candidates above this warp's 32nd best enter its sorted top-32
+            const uint64_t w32 = shfl_idx_u64(wtop[u], 31);
+            uint32_t ins = __ballot_sync(0xffffffffu, cand && key > w32);
+            while (ins) {
+              const int b = __ffs(ins) - 1;
+              ins &= ins - 1;
+              const uint64_t kb = shfl_idx_u64(key, b);
+              if (kb > shfl_idx_u64(wtop[u], 31)) wtop[u] = wlist_insert(wtop[u], kb, lane);
+            }
           }
         }
       }
       if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
     }
+    cp_async_wait<0>();
     __syncwarp();
+    tile = next;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) a[t] = na[t];
+    lw = nlw;
   }
 
   // ---- per-CTA pass counts
@@ -339,37 +469,72 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     if (lane == 0) d = *(volatile int*)&ctl->done;
     d = __shfl_sync(0xffffffffu, d, 0);
     if (d == NW) break;
-    __nanosleep(64);
+    __nanosleep(256);
   }
   __syncthreads();
+  dbg_mark(p.dbg, blockIdx.x * 8 + 1);
 
-  // ---- 4. final per-CTA top-K: select, sort descending, write
+  // ---- 4. per-CTA output: sorted top-32 sample (tree merge of the warp lists) + the buffer
+  uint64_t* wl_smem = reinterpret_cast<uint64_t*>(rings);   // NW x 32 keys (rings are idle now)
+  const size_t cta = (size_t)blockIdx.x;
   for (int u = 0; u < p.nu; ++u) {
+    wl_smem[warp * 32 + lane] = wtop[u];
+    __syncthreads();
+    for (int step = 1; step < NW; step <<= 1) {
+      if ((warp % (2 * step)) == 0 && warp + step < NW) {
+        const uint64_t mine = wl_smem[warp * 32 + lane];
+        const uint64_t other = wl_smem[(warp + step) * 32 + lane];
+        wl_smem[warp * 32 + lane] = wlist_merge(mine, other, lane);
+      }
+      __syncthreads();
+    }
+    uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
+    if (warp == 0) samp[lane] = wl_smem[lane];
+    // the whole buffer (unsorted); compacted to the top-K first if it exceeds the list capacity
     uint64_t* b = bufs + (size_t)u * p.bufcap;
     int n = min(ctl->count[u], p.bufcap);
-    if (n > p.K) {
+    if (n > p.list_cap) {
       const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, p.K, &ctl->sel);
       n = block_compact_ge<NT>(b, n, T, &ctl->sel);
     }
-    const int P2 = next_pow2(n > 1 ? n : 1);
-    for (int i = n + tid; i < P2; i += NT) b[i] = 0ull;
-    __syncthreads();
-    block_sort_desc<NT>(b, P2);
-    uint64_t* out = p.out_keys + ((size_t)u * gridDim.x + blockIdx.x) * p.K;
-    for (int i = tid; i < p.K; i += NT) out[i] = (i < n) ? b[i] : 0ull;
+    uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;
+    for (int i = tid; i < n; i += NT) lst[i] = b[i];
+    if (tid == 0) p.out_cnt[(size_t)u * gridDim.x + cta] = n;
     __syncthreads();
   }
-  if (tid < p.nu) {
-    p.out_pass[(size_t)tid * gridDim.x + blockIdx.x] = (int64_t)ctl->pass[tid];
-  }
+  if (tid < p.nu) p.out_pass[(size_t)tid * gridDim.x + cta] = (int64_t)ctl->pass[tid];
   if (tid == 0 && ctl->overflow) atomicAdd(&p.hdr->overflow, (unsigned long long)ctl->overflow);
+  dbg_mark(p.dbg, blockIdx.x * 8 + 3);
+
+  // ---- 5. fused merge: the last nu CTAs to finish merge one user each (no extra launch)
+  if (!p.fuse_merge) return;
+  __threadfence();   // this CTA's outputs are visible before it takes a ticket
+  __syncthreads();
+  if (tid == 0) ctl->ticket = (int)atomicAdd(&p.hdr->done_ctas, 1u);
+  __syncthreads();
+  const int ticket = ctl->ticket;
+  const int first = (int)gridDim.x - p.nu;
+  if (ticket < first) return;
+  if (tid == 0) {   // wait until every CTA of this launch has published its outputs
+    while (*(volatile unsigned int*)&p.hdr->done_ctas < gridDim.x) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  merge_user<NT>(p.mp, ticket - first, smem_raw);
+  if (tid == 0) {
+    if (atomicAdd(&p.hdr->merged, 1u) == (unsigned int)p.nu - 1) {   // last merger resets the counters
+      p.hdr->merged = 0u;
+      __threadfence();
+      atomicExch(&p.hdr->done_ctas, 0u);
+    }
+  }
 }
 
 template <int DT>
 struct ScanDispatch {
   template <int D, int NQV>
   static constexpr int nt() {
-    return (NQV >= 4 || RowGeom<DT, D>::CPL >= 2) ? 512 : 1024;
+    return 512;   // 16 warps x 128 registers: query chunks + next-tile prefetch stay in registers
   }
   template <int D, int NQV>
   static cudaError_t go(const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
@@ -381,6 +546,8 @@ struct ScanDispatch {
       if (e != cudaSuccess) return e;
       smem_set = smem;
     }
+    // grid = #SMs at one CTA per SM: every CTA is resident, so the fused merge's wait for the
+    // other CTAs of the launch cannot deadlock (CTAs only wait on CTAs of the same launch).
     k<<<grid, NT, smem, st>>>(p);
     return cudaGetLastError();
   }
@@ -406,11 +573,20 @@ struct ScanDispatch {
     }
     return cudaErrorInvalidValue;
   }
+  template <int D, int NQV>
+  static ScanCfg cfg_dq() {
+    using G = RowGeom<DT, D, NQV>;
+    return ScanCfg{nt<D, NQV>(), G::RPI, kStages * G::RPI * G::ROWB};
+  }
   template <int D>
   static ScanCfg cfg_d(int nqv) {
-    using G = RowGeom<DT, D>;
-    int nt = (nqv >= 4 || G::CPL >= 2) ? 512 : 1024;
-    return ScanCfg{nt, G::RPI};
+    switch (nqv) {
+      case 1: return cfg_dq<D, 1>();
+      case 2: return cfg_dq<D, 2>();
+      case 4: return cfg_dq<D, 4>();
+      case 8: return cfg_dq<D, 8>();
+    }
+    return ScanCfg{0, 0, 0};
   }
   static ScanCfg cfg(int dim, int nqv) {
     switch (dim) {
@@ -422,7 +598,7 @@ struct ScanDispatch {
       case 512: return cfg_d<512>(nqv);
       case 1024: return cfg_d<1024>(nqv);
     }
-    return ScanCfg{0, 0};
+    return ScanCfg{0, 0, 0};
   }
 };
 

@@ -23,7 +23,8 @@ ABI_FUNCTIONS = (
     "linr_index_update_rows", "linr_index_delete_rows", "linr_index_stats",
     "linr_search_workspace_bytes", "linr_search", "linr_search_keys", "linr_merge_workspace_bytes",
     "linr_merge_keys", "linr_search_host_extra_bytes", "linr_search_host", "linr_index_generate",
-    "linr_generate_rows", "linr_index_profile", "linr_index_profile_read", "linr_last_error", "linr_version",
+    "linr_generate_rows", "linr_index_profile", "linr_index_profile_read", "linr_debug_timers", "linr_debug_read",
+    "linr_last_error", "linr_version",
 )
 
 
@@ -74,6 +75,8 @@ def library():
         "linr_index_profile": ([P, ctypes.c_int], ctypes.c_int),
         "linr_index_profile_read": ([P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), PI64,
                                      PI64], ctypes.c_int),
+        "linr_debug_timers": ([ctypes.c_int], ctypes.c_int),
+        "linr_debug_read": ([P, I32], ctypes.c_int),
         "linr_last_error": ([], ctypes.c_char_p),
         "linr_version": ([], ctypes.c_int),
     }

@@ -161,26 +161,6 @@ LINR_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "mem
 template <int N>
 LINR_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Insert `k` (> the current 32nd) into a descending 32-list spread over the warp (lane i = rank i).
-LINR_DEV uint64_t wlist_insert(uint64_t wl, uint64_t k, int lane) {
-  const uint64_t up = shfl_up_u64(wl, 1);
-  if (wl > k) return wl;
-  return (lane == 0 || up > k) ? k : up;
-}
-
-// Top-32 of two descending 32-lists a (this lane: a_i) and b (this lane: b_i), descending.
-LINR_DEV uint64_t wlist_merge(uint64_t a, uint64_t b, int lane) {
-  const uint64_t br = shfl_idx_u64(b, 31 - lane);
-  uint64_t c = a > br ? a : br;   // bitonic, holds the top-32 of a U b
-#pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {
-    const uint64_t pc = shfl_xor_u64(c, j);
-    const bool lower = (lane & j) == 0;
-    c = lower ? (c > pc ? c : pc) : (c < pc ? c : pc);
-  }
-  return c;
-}
-
 template <int NT>
 __device__ __noinline__ void scan_compact_all(ScanCtl* ctl, uint64_t* bufs, const ScanParams& p) {
   __syncthreads();   // every warp of the CTA is here (flag checks are warp-uniform)
@@ -202,14 +182,104 @@ __device__ __noinline__ void scan_compact_all(ScanCtl* ctl, uint64_t* bufs, cons
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- tensor-core GEMV geometry
+// bf16/f16 (mma.m16n8k16, fp32 accumulate) and int8 (mma.m16n8k32, exact s32 accumulate): a warp
+// scores 16 gathered rows against up to 8 query vectors (the mma's n = 8 columns) per group. The
+// rows sit in a per-warp shared-memory ring filled by cp.async with an XOR swizzle on the 16-byte
+// chunk index so ldmatrix reads 8 rows at the same column without bank conflicts. The path is
+// HBM-bound; the mma only replaces ~8 CUDA-core instructions per row (unpack + FFMA + butterfly)
+// with ~1 (ldmatrix + mma per 16 rows x 16/32 k), cutting issue pressure. f32 (no exact tensor-core
+// path) and other shapes use the FFMA geometry above.
+template <int DT, int D>
+struct MmaGeom {
+  static constexpr bool ok = ((DT == LINR_BF16 || DT == LINR_F16) && D >= 16 && D <= 128) ||
+                             (DT == LINR_I8 && D >= 32 && D <= 256);
+  static constexpr int ESZ = (DT == LINR_I8) ? 1 : 2;
+  static constexpr int ROWB = D * ESZ;
+  static constexpr int CH = ROWB / 16;           // 16-byte chunks per row
+  static constexpr int NKS = ROWB / 32;          // k-steps of 32 bytes (k16 bf16 / k32 int8)
+  static constexpr int ROWS = 16;                // rows per group
+  static constexpr int STAGE = ROWS * ROWB;
+  static constexpr int S0 = 8192 / (STAGE > 0 ? STAGE : 1);
+  static constexpr int S = S0 < 2 ? 2 : (S0 > 4 ? 4 : S0);   // ring stages
+  static constexpr int CPLN = (ROWS * CH) / 32 > 0 ? (ROWS * CH) / 32 : 1;   // chunks per lane per stage
+  static constexpr int SWZ_DIV = CH >= 8 ? 1 : 8 / (CH > 0 ? CH : 1);
+  static constexpr int SWZ_MOD = CH >= 8 ? 8 : CH;
+  LINR_DEV static int swz(int row) { return (row / SWZ_DIV) % (SWZ_MOD > 0 ? SWZ_MOD : 1); }
+};
+
+LINR_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+template <int DT>
+LINR_DEV void mma16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (DT == LINR_BF16) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  } else {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+}
+LINR_DEV void mma32_s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NT, int NU>
+struct Appender {
+  // Threshold test + warp-aggregated append of candidate keys into the CTA buffer of user u.
+  LINR_DEV static void append(ScanCtl* ctl, uint64_t* bufs, const ScanParams& p, int u, bool cand_in, uint64_t key) {
+    const int lane = threadIdx.x & 31;
+    bool cand = cand_in && key >= *(volatile const unsigned long long*)&ctl->thr[u];
+    const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+    if (!bal) return;
+    const int leader = __ffs(bal) - 1;
+    const int nb = __popc(bal);
+    int pos0 = 0;
+    if (lane == leader) {
+      pos0 = atomicAdd(&ctl->count[u], nb);
+      if (pos0 + nb >= p.C) {
+        *(volatile int*)&ctl->flag = 1;
+        __threadfence_block();
+      }
+    }
+    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (cand) {
+      const int pos = pos0 + __popc(bal & lanemask_lt());
+      if (pos < p.bufcap) bufs[(size_t)u * p.bufcap + pos] = key;
+      else atomicAdd(&ctl->overflow, 1);
+    }
+  }
+};
+
+template <int DT, int D, int NQV>
+struct ScanGeom {
+  static constexpr bool kMma = MmaGeom<DT, D>::ok && NQV <= 8;
+  static constexpr int RPI = kMma ? 16 : RowGeom<DT, D, NQV>::RPI;   // rows per warp iteration
+  static constexpr int RING = kMma ? MmaGeom<DT, D>::S * MmaGeom<DT, D>::STAGE
+                                   : kStages * RowGeom<DT, D, NQV>::RPI * RowGeom<DT, D, NQV>::ROWB;
+};
+
 template <int DT, int D, int NQV, int NT>
 __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant__ ScanParams p) {
   using G = RowGeom<DT, D, NQV>;
+  using M = MmaGeom<DT, D>;
+  constexpr bool kMma = ScanGeom<DT, D, NQV>::kMma;
   constexpr bool kInt = (DT == LINR_I8);
   using acc_t = typename std::conditional<kInt, int, float>::type;
   constexpr int NW = NT / 32;
   constexpr int NU = NQV;   // at most one user per vector
-  constexpr int STAGE = G::RPI * G::ROWB;   // bytes of one ring stage
+  constexpr int RING = ScanGeom<DT, D, NQV>::RING;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScanCtl* ctl = reinterpret_cast<ScanCtl*>(smem_raw);
@@ -218,7 +288,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   uint16_t* wlist_all = reinterpret_cast<uint16_t*>(bufs + (size_t)p.nu * p.bufcap);
   uint16_t* wlist = wlist_all + warp * kTileItems;
   unsigned char* rings = reinterpret_cast<unsigned char*>(wlist_all + NW * kTileItems);   // 16B aligned
-  unsigned char* ring = rings + (size_t)warp * kStages * STAGE;
+  unsigned char* ring = rings + (size_t)warp * RING;
 
   if (tid < kMaxUsers) {
     ctl->thr[tid] = 0ull;
@@ -227,27 +297,50 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   }
   if (tid == 0) { ctl->flag = 0; ctl->done = 0; ctl->overflow = 0; ctl->next_tile = 0; }
 
-  // ---- query chunks into registers (lane group member gl owns chunks gl + c*LPR)
-  const int g = lane / G::LPR, gl = lane % G::LPR;
   const int nvec = p.nu * p.V;
+  // ---- query registers
+  // FFMA path: lane group member gl owns chunks gl + c*LPR of every query vector.
+  // MMA path: B fragments; lane (g = lane/4, t = lane%4) holds vector g's k-pairs 2t, 2t+8 (bf16)
+  // or k-quads 4t, 4t+16 (int8) of every k-step.
+  const int g = lane / G::LPR, gl = lane % G::LPR;
   int uj[NQV];
 #pragma unroll
   for (int j = 0; j < NQV; ++j) uj[j] = (j < nvec) ? j / p.V : -1;
-
-  float qf[kInt ? 1 : NQV][kInt ? 1 : G::CPL][kInt ? 1 : G::EPC];
-  uint4 qi[kInt ? NQV : 1][kInt ? G::CPL : 1];
+  float qf[(kInt || kMma) ? 1 : NQV][(kInt || kMma) ? 1 : G::CPL][(kInt || kMma) ? 1 : G::EPC];
+  uint4 qi[(kInt && !kMma) ? NQV : 1][(kInt && !kMma) ? G::CPL : 1];
+  uint32_t bq[kMma ? M::NKS : 1][2];
+  int ucol0 = -1, ucol1 = -1;   // MMA path: user of this lane's two accumulator columns
+  if constexpr (kMma) {
+    const int mg = lane >> 2, mt = lane & 3;
+    ucol0 = (2 * mt < nvec) ? (2 * mt) / p.V : -1;
+    ucol1 = (2 * mt + 1 < nvec) ? (2 * mt + 1) / p.V : -1;
+    const char* qv = reinterpret_cast<const char*>(p.q) + (size_t)mg * M::ROWB;
 #pragma unroll
-  for (int j = 0; j < NQV; ++j) {
+    for (int ks = 0; ks < M::NKS; ++ks) {
+      uint32_t b0 = 0, b1 = 0;
+      if (mg < nvec) {
+        const int o0 = kInt ? (ks * 32 + 4 * mt) : (ks * 16 + 2 * mt) * 2;
+        const int o1 = kInt ? (ks * 32 + 4 * mt + 16) : (ks * 16 + 2 * mt + 8) * 2;
+        b0 = __ldg(reinterpret_cast<const unsigned int*>(qv + o0));
+        b1 = __ldg(reinterpret_cast<const unsigned int*>(qv + o1));
+      }
+      bq[ks][0] = b0;
+      bq[ks][1] = b1;
+    }
+  } else {
 #pragma unroll
-    for (int c = 0; c < G::CPL; ++c) {
-      uint4 raw = make_uint4(0, 0, 0, 0);
-      if (j < nvec)
-        raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.q) + (size_t)j * G::ROWB +
-                                                   (gl + c * G::LPR) * 16));
-      if constexpr (kInt) {
-        qi[j][c] = raw;
-      } else {
-        ChunkDot<DT>::load_q(raw, qf[j][c]);
+    for (int j = 0; j < NQV; ++j) {
+#pragma unroll
+      for (int c = 0; c < G::CPL; ++c) {
+        uint4 raw = make_uint4(0, 0, 0, 0);
+        if (j < nvec)
+          raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.q) + (size_t)j * G::ROWB +
+                                                     (gl + c * G::LPR) * 16));
+        if constexpr (kInt) {
+          qi[j][c] = raw;
+        } else {
+          ChunkDot<DT>::load_q(raw, qf[j][c]);
+        }
       }
     }
   }
@@ -276,9 +369,8 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   };
 
   uint32_t pcnt[NU];
-  uint64_t wtop[NU];   // this warp's sorted top-32 per user (lane i = rank i)
 #pragma unroll
-  for (int u = 0; u < NU; ++u) { pcnt[u] = 0; wtop[u] = 0ull; }
+  for (int u = 0; u < NU; ++u) pcnt[u] = 0;
 
   int64_t tile = grab();
   uint64_t a[8];
@@ -345,102 +437,132 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     for (int u = 0; u < NU; ++u) pcnt[u] += __popc(pb[u]);
     __syncwarp();
 
-    // ---- 2. gather passing rows through the cp.async ring
-    const int n_iter = (cnt + G::RPI - 1) / G::RPI;
-    auto issue = [&](int it) {
-      unsigned char* st = ring + (it % kStages) * STAGE;
+    if constexpr (kMma) {
+      // ---- 2./3. tensor-core path: 16-row groups through the swizzled cp.async ring
+      const int ngrp = (cnt + M::ROWS - 1) / M::ROWS;
+      auto issue = [&](int gi) {
+        unsigned char* st = ring + (gi % M::S) * M::STAGE;
 #pragma unroll
-      for (int r = 0; r < G::R; ++r) {
-        const int slot = r * G::RPW + g;
-        const int idx = it * G::RPI + slot;
-        const uint32_t e = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
-        const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * G::ROWB + gl * 16;
-#pragma unroll
-        for (int c = 0; c < G::CPL; ++c)
-          cp_async16(st + slot * G::ROWB + (gl + c * G::LPR) * 16, src + c * G::LPR * 16, e ? 16 : 0);
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int it = 0; it < kStages - 1; ++it) {
-      if (it < n_iter) issue(it); else cp_async_commit();
-    }
-    for (int it = 0; it < n_iter; ++it) {
-      if (it + kStages - 1 < n_iter) issue(it + kStages - 1); else cp_async_commit();
-      cp_async_wait<kStages - 1>();
-      const unsigned char* st = ring + (it % kStages) * STAGE;
-#pragma unroll
-      for (int r = 0; r < G::R; ++r) {
-        const int slot = r * G::RPW + g;
-        const int idx = it * G::RPI + slot;
-        const uint32_t ent = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
-        uint4 v[G::CPL];
-#pragma unroll
-        for (int c = 0; c < G::CPL; ++c)
-          v[c] = *reinterpret_cast<const uint4*>(st + slot * G::ROWB + (gl + c * G::LPR) * 16);
-        acc_t s[NQV];
-#pragma unroll
-        for (int j = 0; j < NQV; ++j) {
-          acc_t acc = 0;
-#pragma unroll
-          for (int c = 0; c < G::CPL; ++c) {
-            if constexpr (kInt) {
-              acc = __dp4a((int)v[c].x, (int)qi[j][c].x, acc);
-              acc = __dp4a((int)v[c].y, (int)qi[j][c].y, acc);
-              acc = __dp4a((int)v[c].z, (int)qi[j][c].z, acc);
-              acc = __dp4a((int)v[c].w, (int)qi[j][c].w, acc);
-            } else {
-              acc = ChunkDot<DT>::dot(v[c], qf[j][c], acc);
-            }
-          }
-#pragma unroll
-          for (int o = G::LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          s[j] = acc;
+        for (int j = 0; j < M::CPLN; ++j) {
+          const int q = lane + 32 * j;
+          const int row = q / M::CH, c = q % M::CH;
+          const int idx = gi * M::ROWS + row;
+          const uint32_t e = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+          const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * M::ROWB + c * 16;
+          cp_async16(st + row * M::ROWB + ((c ^ M::swz(row)) * 16), src, e ? 16 : 0);
         }
-        const uint32_t gid = p.row0 + (uint32_t)(base + (ent >> 8));
+        cp_async_commit();
+      };
 #pragma unroll
-        for (int u = 0; u < NU; ++u) {
-          float su = -INFINITY;
+      for (int gi = 0; gi < M::S - 1; ++gi) {
+        if (gi < ngrp) issue(gi); else cp_async_commit();
+      }
+      const int mg = lane >> 2, mt = lane & 3;
+      for (int gi = 0; gi < ngrp; ++gi) {
+        if (gi + M::S - 1 < ngrp) issue(gi + M::S - 1); else cp_async_commit();
+        cp_async_wait<M::S - 1>();
+        __syncwarp();   // the group's rows were copied by every lane of the warp
+        const unsigned char* st = ring + (gi % M::S) * M::STAGE;
+        const uint32_t st_s = (uint32_t)__cvta_generic_to_shared(st);
+        acc_t acc[4] = {0, 0, 0, 0};
+        const int lrow = lane & 15, lhalf = lane >> 4;
 #pragma unroll
-          for (int j = 0; j < NQV; ++j)
-            if (uj[j] == u) su = fmaxf(su, (float)s[j]);
-          bool cand = false;
-          uint64_t key = 0ull;
-          if (u < p.nu && gl == 0 && ((ent >> u) & 1u)) {
-            key = make_key(su, gid);
-            cand = key >= *(volatile const unsigned long long*)&ctl->thr[u];
+        for (int ks = 0; ks < M::NKS; ++ks) {
+          uint32_t af[4];
+          const int chunk = ks * 2 + lhalf;
+          ldsm_x4(st_s + lrow * M::ROWB + ((chunk ^ M::swz(lrow)) * 16), af[0], af[1], af[2], af[3]);
+          if constexpr (kInt) mma32_s8(acc, af, bq[ks][0], bq[ks][1]);
+          else mma16<DT>(acc, af, bq[ks][0], bq[ks][1]);
+        }
+        // accumulator: acc[0..1] = row mg, columns 2mt, 2mt+1; acc[2..3] = row mg+8
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = mg + 8 * h;
+          const int idx = gi * M::ROWS + row;
+          const uint32_t ent = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+          const uint32_t gid = p.row0 + (uint32_t)(base + (ent >> 8));
+          const float v0 = (float)acc[2 * h], v1 = (float)acc[2 * h + 1];
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            float m = -INFINITY;
+            if (ucol0 == u) m = v0;
+            if (ucol1 == u) m = fmaxf(m, v1);
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+            const bool cand = u < p.nu && mt == 0 && ((ent >> u) & 1u);
+            Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(m, gid) : 0ull);
           }
-          const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-          if (bal) {
-            const int leader = __ffs(bal) - 1;
-            const int nb = __popc(bal);
-            int pos0 = 0;
-            if (lane == leader) {
-              pos0 = atomicAdd(&ctl->count[u], nb);
-              if (pos0 + nb >= p.C) {
-                *(volatile int*)&ctl->flag = 1;
-                __threadfence_block();
+        }
+        __syncwarp();   // every lane is done reading this stage before it is refilled
+        if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
+      }
+    } else {
+      // ---- 2./3. CUDA-core path: LPR lanes per row, cp.async ring of kStages stages
+      const int n_iter = (cnt + G::RPI - 1) / G::RPI;
+      constexpr int STAGE = G::RPI * G::ROWB;
+      auto issue = [&](int it) {
+        unsigned char* st = ring + (it % kStages) * STAGE;
+#pragma unroll
+        for (int r = 0; r < G::R; ++r) {
+          const int slot = r * G::RPW + g;
+          const int idx = it * G::RPI + slot;
+          const uint32_t e = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+          const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * G::ROWB + gl * 16;
+#pragma unroll
+          for (int c = 0; c < G::CPL; ++c)
+            cp_async16(st + slot * G::ROWB + (gl + c * G::LPR) * 16, src + c * G::LPR * 16, e ? 16 : 0);
+        }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int it = 0; it < kStages - 1; ++it) {
+        if (it < n_iter) issue(it); else cp_async_commit();
+      }
+      for (int it = 0; it < n_iter; ++it) {
+        if (it + kStages - 1 < n_iter) issue(it + kStages - 1); else cp_async_commit();
+        cp_async_wait<kStages - 1>();   // each lane reads back only the chunks it copied
+        const unsigned char* st = ring + (it % kStages) * STAGE;
+#pragma unroll
+        for (int r = 0; r < G::R; ++r) {
+          const int slot = r * G::RPW + g;
+          const int idx = it * G::RPI + slot;
+          const uint32_t ent = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
+          uint4 v[G::CPL];
+#pragma unroll
+          for (int c = 0; c < G::CPL; ++c)
+            v[c] = *reinterpret_cast<const uint4*>(st + slot * G::ROWB + (gl + c * G::LPR) * 16);
+          acc_t s[NQV];
+#pragma unroll
+          for (int j = 0; j < NQV; ++j) {
+            acc_t acc = 0;
+#pragma unroll
+            for (int c = 0; c < G::CPL; ++c) {
+              if constexpr (kInt) {
+                acc = __dp4a((int)v[c].x, (int)qi[j][c].x, acc);
+                acc = __dp4a((int)v[c].y, (int)qi[j][c].y, acc);
+                acc = __dp4a((int)v[c].z, (int)qi[j][c].z, acc);
+                acc = __dp4a((int)v[c].w, (int)qi[j][c].w, acc);
+              } else {
+                acc = ChunkDot<DT>::dot(v[c], qf[j][c], acc);
               }
             }
-            pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-            if (cand) {
-              const int pos = pos0 + __popc(bal & lanemask_lt());
-              if (pos < p.bufcap) bufs[(size_t)u * p.bufcap + pos] = key;
-              else atomicAdd(&ctl->overflow, 1);
-            }
-            // warp select: candidates above this warp's 32nd best enter its sorted top-32
-            const uint64_t w32 = shfl_idx_u64(wtop[u], 31);
-            uint32_t ins = __ballot_sync(0xffffffffu, cand && key > w32);
-            while (ins) {
-              const int b = __ffs(ins) - 1;
-              ins &= ins - 1;
-              const uint64_t kb = shfl_idx_u64(key, b);
-              if (kb > shfl_idx_u64(wtop[u], 31)) wtop[u] = wlist_insert(wtop[u], kb, lane);
-            }
+#pragma unroll
+            for (int o = G::LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            s[j] = acc;
+          }
+          const uint32_t gid = p.row0 + (uint32_t)(base + (ent >> 8));
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            float su = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < NQV; ++j)
+              if (uj[j] == u) su = fmaxf(su, (float)s[j]);
+            const bool cand = u < p.nu && gl == 0 && ((ent >> u) & 1u);
+            Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(su, gid) : 0ull);
           }
         }
+        if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
       }
-      if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
     }
     cp_async_wait<0>();
     __syncwarp();
@@ -474,28 +596,41 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   __syncthreads();
   dbg_mark(p.dbg, blockIdx.x * 8 + 1);
 
-  // ---- 4. per-CTA output: sorted top-32 sample (tree merge of the warp lists) + the buffer
-  uint64_t* wl_smem = reinterpret_cast<uint64_t*>(rings);   // NW x 32 keys (rings are idle now)
+  // ---- 4. per-CTA output: sorted top-32 sample + the whole (unsorted) buffer
+  uint64_t* scratch64 = reinterpret_cast<uint64_t*>(rings);   // 64 keys (the rings are idle now)
   const size_t cta = (size_t)blockIdx.x;
   for (int u = 0; u < p.nu; ++u) {
-    wl_smem[warp * 32 + lane] = wtop[u];
-    __syncthreads();
-    for (int step = 1; step < NW; step <<= 1) {
-      if ((warp % (2 * step)) == 0 && warp + step < NW) {
-        const uint64_t mine = wl_smem[warp * 32 + lane];
-        const uint64_t other = wl_smem[(warp + step) * 32 + lane];
-        wl_smem[warp * 32 + lane] = wlist_merge(mine, other, lane);
-      }
-      __syncthreads();
-    }
-    uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
-    if (warp == 0) samp[lane] = wl_smem[lane];
-    // the whole buffer (unsorted); compacted to the top-K first if it exceeds the list capacity
     uint64_t* b = bufs + (size_t)u * p.bufcap;
     int n = min(ctl->count[u], p.bufcap);
     if (n > p.list_cap) {
       const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, p.K, &ctl->sel);
       n = block_compact_ge<NT>(b, n, T, &ctl->sel);
+    }
+    // sample: the top-32 keys, sorted
+    if (n > kSample) {
+      const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
+      if (tid == 0) ctl->wcnt = 0;
+      __syncthreads();
+      for (int i0 = 0; i0 < n; i0 += NT) {
+        const int i = i0 + tid;
+        const bool top = i < n && b[i] >= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, top);
+        int at = 0;
+        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (top) scratch64[at + __popc(bal & lanemask_lt())] = b[i];
+      }
+      __syncthreads();
+    } else {
+      for (int i = tid; i < kSample; i += NT) scratch64[i] = i < n ? b[i] : 0ull;
+      __syncthreads();
+    }
+    uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
+    if (warp == 0) {
+      scratch64[32 + lane] = 0ull;
+      __syncwarp();
+      warp_sort64_desc(scratch64);
+      samp[lane] = scratch64[lane];
     }
     uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;
     for (int i = tid; i < n; i += NT) lst[i] = b[i];
@@ -575,8 +710,8 @@ struct ScanDispatch {
   }
   template <int D, int NQV>
   static ScanCfg cfg_dq() {
-    using G = RowGeom<DT, D, NQV>;
-    return ScanCfg{nt<D, NQV>(), G::RPI, kStages * G::RPI * G::ROWB};
+    using SG = ScanGeom<DT, D, NQV>;
+    return ScanCfg{nt<D, NQV>(), SG::RPI, SG::RING};
   }
   template <int D>
   static ScanCfg cfg_d(int nqv) {

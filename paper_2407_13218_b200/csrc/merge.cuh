@@ -89,12 +89,13 @@ __device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
   const int DB = 4096 + u * 8;
   dbg_mark(p.dbg, DB + 0);
 
-  if (tid == 0) { ctl->nnz = 0; ctl->cnt = 0; }
-  if (warp == 0) {
+  if (tid == 0) { ctl->nnz = 0; ctl->cnt = 0; ctl->pass = 0; }
+  __syncthreads();
+  {   // pass counts: all loads in flight at once
     long long acc = 0;
-    for (int l = lane; l < L; l += 32) acc += p.pass[(int64_t)l * p.pstride_l + (int64_t)u * p.pstride_u];
+    for (int l = tid; l < L; l += NT) acc += p.pass[(int64_t)l * p.pstride_l + (int64_t)u * p.pstride_u];
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) ctl->pass = acc;
+    if (lane == 0 && acc) atomicAdd((unsigned long long*)&ctl->pass, (unsigned long long)acc);
   }
   auto lcount = [cntp, csl, len](int l) -> int { return cntp ? cntp[(int64_t)l * csl] : len; };
   __syncthreads();

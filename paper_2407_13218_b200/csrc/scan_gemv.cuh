@@ -372,16 +372,19 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
 #pragma unroll
   for (int u = 0; u < NU; ++u) pcnt[u] = 0;
 
+  // attribute words + liveness of the next two tiles are in flight while a tile is processed
   int64_t tile = grab();
-  uint64_t a[8];
-  uint32_t lw = 0;
+  uint64_t a[8], na[8];
+  uint32_t lw = 0, nlw = 0;
   if (tile < t_end) prefetch(tile, a, lw);
+  int64_t next = grab();
+  if (next < t_end) prefetch(next, na, nlw);
   while (tile < t_end) {
     if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
-    const int64_t next = grab();
-    uint64_t na[8];
-    uint32_t nlw = 0;
-    if (next < t_end) prefetch(next, na, nlw);
+    const int64_t next2 = grab();
+    uint64_t nna[8];
+    uint32_t nnlw = 0;
+    if (next2 < t_end) prefetch(next2, nna, nnlw);
     const int64_t base = tile * kTileItems;
 
     // ---- 1. liveness + clauses -> pass bits
@@ -440,16 +443,30 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     if constexpr (kMma) {
       // ---- 2./3. tensor-core path: 16-row groups through the swizzled cp.async ring
       const int ngrp = (cnt + M::ROWS - 1) / M::ROWS;
+      // copy mapping: LPRC lanes per row, each copying CPR chunks (chunk cl + k*LPRC), so one
+      // instruction moves LPRC*16 contiguous bytes of each of 32/LPRC rows (full 32-byte sectors);
+      // one wlist lookup and one base address per row per lane.
+      constexpr int LPRC = M::CH < 4 ? M::CH : 4;
+      constexpr int RPS = 32 / LPRC;                 // rows per copy step
+      constexpr int NRS = M::ROWS / RPS;             // copy steps per group
+      constexpr int CPR = M::CH / LPRC;              // chunks per lane per row
+      const int crow = lane / LPRC, cl = lane % LPRC;
       auto issue = [&](int gi) {
         unsigned char* st = ring + (gi % M::S) * M::STAGE;
 #pragma unroll
-        for (int j = 0; j < M::CPLN; ++j) {
-          const int q = lane + 32 * j;
-          const int row = q / M::CH, c = q % M::CH;
+        for (int rs = 0; rs < NRS; ++rs) {
+          const int row = crow + rs * RPS;
           const int idx = gi * M::ROWS + row;
           const uint32_t e = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
-          const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * M::ROWB + c * 16;
-          cp_async16(st + row * M::ROWB + ((c ^ M::swz(row)) * 16), src, e ? 16 : 0);
+          const char* src = reinterpret_cast<const char*>(p.emb) + (size_t)(base + (e >> 8)) * M::ROWB;
+          unsigned char* dst = st + row * M::ROWB;
+          const int sw = M::swz(row);
+          const int bytes = e ? 16 : 0;
+#pragma unroll
+          for (int k = 0; k < CPR; ++k) {
+            const int c = cl + k * LPRC;
+            cp_async16(dst + ((c ^ sw) * 16), src + c * 16, bytes);
+          }
         }
         cp_async_commit();
       };
@@ -482,15 +499,20 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
           const uint32_t ent = (idx < cnt) ? (uint32_t)wlist[idx] : 0u;
           const uint32_t gid = p.row0 + (uint32_t)(base + (ent >> 8));
           const float v0 = (float)acc[2 * h], v1 = (float)acc[2 * h + 1];
+          if constexpr (NQV == 1) {   // one user, one vector: column 0 lives in lanes mt == 0
+            const bool cand = p.nu > 0 && mt == 0 && (ent & 1u);
+            Appender<NT, NU>::append(ctl, bufs, p, 0, cand, cand ? make_key(v0, gid) : 0ull);
+          } else {
 #pragma unroll
-          for (int u = 0; u < NU; ++u) {
-            float m = -INFINITY;
-            if (ucol0 == u) m = v0;
-            if (ucol1 == u) m = fmaxf(m, v1);
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-            const bool cand = u < p.nu && mt == 0 && ((ent >> u) & 1u);
-            Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(m, gid) : 0ull);
+            for (int u = 0; u < NU; ++u) {
+              float m = -INFINITY;
+              if (ucol0 == u) m = v0;
+              if (ucol1 == u) m = fmaxf(m, v1);
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+              const bool cand = u < p.nu && mt == 0 && ((ent >> u) & 1u);
+              Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(m, gid) : 0ull);
+            }
           }
         }
         __syncwarp();   // every lane is done reading this stage before it is refilled
@@ -567,9 +589,14 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
     cp_async_wait<0>();
     __syncwarp();
     tile = next;
+    next = next2;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) a[t] = na[t];
+    for (int t = 0; t < 8; ++t) {
+      a[t] = na[t];
+      na[t] = nna[t];
+    }
     lw = nlw;
+    nlw = nnlw;
   }
 
   // ---- per-CTA pass counts

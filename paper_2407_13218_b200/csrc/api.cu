@@ -74,9 +74,17 @@ struct ProfEvents {
 
 struct linr_index {
   linr_index_desc d;
+  // batched tcgen05 path state
+  CUtensorMap tmx;
+  bool tmx_ok = false;
+  void* pin = nullptr;          // pinned staging for clauses / flags
+  size_t pin_bytes = 0;
+  cudaEvent_t pin_ev = nullptr;
   bool prof = false;
   std::vector<ProfEvents> prof_used, prof_free;
   int64_t prof_launches = 0;
+  int64_t tc_fallbacks = 0;     // batched-path users recomputed on the GEMV path
+  bool force_gemv = false;
   int64_t cap_pad;
   int rowbytes;
   int num_sms;
@@ -172,6 +180,171 @@ WsLayout ws_layout(const Plan& pl, int B, int K) {
   return w;
 }
 
+
+// ----------------------------------------------------------------- batched tcgen05 path
+struct TcWs {
+  size_t sbuf, scnt, thr, mbuf, mcnt, flags, cl, ncl, gemv, end;
+};
+bool use_tc(const linr_index* ix, int B, int V) {
+  return B * V >= 16 && tc_supported(ix->d.dtype, ix->d.dim, B * V) &&
+         tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B) <= ix->smem_optin;
+}
+bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
+  Plan g;
+  if (!make_plan(ix, 1, V, K, &g, why)) return false;   // exact GEMV fallback for uncertified users
+  const size_t nu = (size_t)B;
+  w->sbuf = 0;
+  w->scnt = align256(w->sbuf + nu * kTcSampleCap * 8);
+  w->thr = align256(w->scnt + nu * 4);
+  w->mbuf = align256(w->thr + nu * 8);
+  w->mcnt = align256(w->mbuf + nu * kTcMainCap * 8);
+  w->flags = align256(w->mcnt + nu * 4);
+  w->cl = align256(w->flags + nu * 4);
+  w->ncl = align256(w->cl + nu * 16 * sizeof(KClause));
+  w->gemv = align256(w->ncl + nu * 4);
+  w->end = w->gemv + ws_layout(g, 1, K).end;
+  return true;
+}
+
+int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
+                void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
+                int64_t* out_pass, cudaStream_t st);
+
+int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
+              void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
+              int64_t* out_pass, cudaStream_t st) {
+  std::string why;
+  TcWs w;
+  if (!tc_layout(ix, B, V, K, &w, &why)) return fail(LINR_EUNSUPPORTED, why);
+  if (!ws || ws_bytes < w.end) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+  const int nvec = B * V, np = tc_np(nvec);
+  char* W = (char*)ws;
+  if (!ix->tmx_ok) {
+    ix->tmx_ok = tc_encode_map(&ix->tmx, ix->emb, ix->cap_pad, ix->rowbytes, 128);
+    if (!ix->tmx_ok) return fail(LINR_ECUDA, "cuTensorMapEncodeTiled failed for the item matrix");
+  }
+  TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.tmx = ix->tmx;
+  if (!tc_encode_map(&p.tmq, q, nvec, ix->rowbytes, np)) return fail(LINR_ECUDA, "cuTensorMapEncodeTiled failed for the queries");
+  // clauses: host -> pinned staging -> device (clause lists are host memory per the ABI)
+  const size_t clb = (size_t)B * 16 * sizeof(KClause), nclb = (size_t)B * 4, flb = (size_t)B * 4;
+  const size_t need = clb + nclb + flb;
+  if (!ix->pin_ev) cudaEventCreateWithFlags(&ix->pin_ev, cudaEventDisableTiming);
+  if (ix->pin_bytes < need) {
+    if (ix->pin) {
+      cudaEventSynchronize(ix->pin_ev);
+      cudaFreeHost(ix->pin);
+    }
+    ix->pin = nullptr;
+    if (cudaHostAlloc(&ix->pin, need, cudaHostAllocDefault) != cudaSuccess) return fail(LINR_ENOMEM, "pinned staging");
+    ix->pin_bytes = need;
+  } else {
+    cudaEventSynchronize(ix->pin_ev);   // the previous copy out of the staging buffer is done
+  }
+  KClause* hcl = (KClause*)ix->pin;
+  int* hncl = (int*)((char*)ix->pin + clb);
+  int* hflags = (int*)((char*)ix->pin + clb + nclb);
+  std::memset(hcl, 0, clb);
+  uint32_t wmask = 0;
+  for (int b = 0; b < B; ++b) {
+    hncl[b] = off[b + 1] - off[b];
+    for (int c = 0; c < hncl[b]; ++c) {
+      const linr_clause& k = cl[off[b] + c];
+      hcl[b * 16 + c].mask = k.mask;
+      hcl[b * 16 + c].word = k.word;
+      hcl[b * 16 + c].rev = k.reverse;
+      wmask |= 1u << k.word;
+    }
+  }
+  e = cudaMemcpyAsync(W + w.cl, hcl, clb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(W + w.ncl, hncl, nclb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(ix->pin_ev, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(W + w.scnt, 0, (size_t)B * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "batched staging");
+
+  ProfEvents pe{};
+  if (ix->prof) {
+    if (!ix->prof_free.empty()) {
+      pe = ix->prof_free.back();
+      ix->prof_free.pop_back();
+    } else {
+      cudaEventCreate(&pe.e0);
+      cudaEventCreate(&pe.e1);
+      cudaEventCreate(&pe.e2);
+    }
+    cudaEventRecord(pe.e0, st);
+  }
+  p.attr = ix->attr;
+  p.cap_pad = ix->cap_pad;
+  p.live = ix->live;
+  p.hdr = ix->hdr;
+  p.row0 = (uint32_t)ix->d.global_row0;
+  p.nu = B;
+  p.V = V;
+  p.nvec = nvec;
+  p.K = K;
+  p.wmask = wmask;
+  p.cl = (const KClause*)(W + w.cl);
+  p.ncl = (const int*)(W + w.ncl);
+  // 1. sample pass (no threshold)
+  p.thr = nullptr;
+  p.buf = (uint64_t*)(W + w.sbuf);
+  p.cap = kTcSampleCap;
+  p.cnt = (int*)(W + w.scnt);
+  p.sample_tiles = kTcSampleTiles;
+  e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc sample launch");
+  // 2. thresholds
+  e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, B, K,
+                          ix->num_sms * kTcSampleTiles * 128, ix->hdr, (uint64_t*)(W + w.thr), (int*)(W + w.mcnt), st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc threshold launch");
+  // 3. main pass
+  p.thr = (const uint64_t*)(W + w.thr);
+  p.buf = (uint64_t*)(W + w.mbuf);
+  p.cap = kTcMainCap;
+  p.cnt = (int*)(W + w.mcnt);
+  p.sample_tiles = 0;
+  e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc main launch");
+  if (ix->prof) cudaEventRecord(pe.e1, st);
+  // 4. finalize
+  e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), kTcMainCap,
+                         (const uint64_t*)(W + w.thr), B, K, mode == 0 ? out_ids : nullptr,
+                         mode == 0 ? out_scores : nullptr, mode == 1 ? out_keys : nullptr, (int*)(W + w.flags), st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc finalize launch");
+  if (out_pass) {
+    e = cudaMemsetAsync(out_pass, 0, (size_t)B * 8, st);
+    if (e == cudaSuccess)
+      e = launch_tc_count(ix->attr, ix->cap_pad, ix->live, ix->hdr, p.cl, p.ncl, B, (unsigned long long*)out_pass,
+                          ix->num_sms * 4, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tc pass-count launch");
+  }
+  if (ix->prof) {
+    cudaEventRecord(pe.e2, st);
+    ix->prof_used.push_back(pe);
+    ix->prof_launches += 4 + (out_pass ? 1 : 0);
+  }
+  // 5. certify: users whose result is not provably exact are recomputed on the exact GEMV path
+  e = cudaMemcpyAsync(hflags, W + w.flags, flb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc flags");
+  for (int b = 0; b < B; ++b) {
+    if (!hflags[b]) continue;
+    const int32_t off1[2] = {0, off[b + 1] - off[b]};
+    const int rc = search_impl(ix, (const char*)q + (size_t)b * V * ix->rowbytes, 1, V, cl + off[b], off1, K,
+                               W + w.gemv, ws_bytes - w.gemv, mode, out_ids ? out_ids + (size_t)b * K : nullptr,
+                               out_scores ? out_scores + (size_t)b * K : nullptr,
+                               out_keys ? out_keys + (size_t)b * K : nullptr, out_pass ? out_pass + b : nullptr, st);
+    if (rc != LINR_OK) return rc;
+    ix->tc_fallbacks++;
+  }
+  return LINR_OK;
+}
+
 int validate_query(const linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off,
                    int K, std::string* why) {
   if (!ix) { *why = "null index"; return LINR_EINVAL; }
@@ -204,6 +377,8 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   if (rc != LINR_OK) return fail(rc, why);
   if (mode == 0 && (!out_ids || !out_scores)) return fail(LINR_EINVAL, "null outputs");
   if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
+  if (use_tc(ix, B, V) && !ix->force_gemv)
+    return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
   Plan pl;
   if (!make_plan(ix, B, V, K, &pl, &why)) return fail(LINR_EUNSUPPORTED, why);
   const WsLayout wl = ws_layout(pl, B, K);
@@ -391,6 +566,8 @@ int linr_index_create(const linr_index_desc* d, linr_index** out) {
 
 void linr_index_destroy(linr_index* ix) {
   if (!ix) return;
+  if (ix->pin) cudaFreeHost(ix->pin);
+  if (ix->pin_ev) cudaEventDestroy(ix->pin_ev);
   for (auto* v : {&ix->prof_used, &ix->prof_free})
     for (auto& pe : *v) {
       cudaEventDestroy(pe.e0);
@@ -493,8 +670,13 @@ size_t linr_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, i
   if (!ix || B < 1 || V < 1 || V > 8 || K < 1 || K > LINR_MAX_K) return 0;
   Plan pl;
   std::string why;
-  if (!make_plan(ix, B, V, K, &pl, &why)) return 0;
-  return ws_layout(pl, B, K).end;
+  size_t n = 0;
+  if (use_tc(ix, B, V)) {
+    TcWs w;
+    if (tc_layout(ix, B, V, K, &w, &why)) n = w.end;
+  }
+  if (make_plan(ix, B, V, K, &pl, &why)) n = std::max(n, ws_layout(pl, B, K).end);
+  return n;
 }
 
 int linr_search(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,

@@ -1,5 +1,6 @@
 // Internal declarations shared by the library's translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -103,6 +104,43 @@ cudaError_t launch_delete_rows(const int64_t* rows, int64_t n, int64_t grow0, in
 cudaError_t launch_generate(int dtype, int dim, int W, uint64_t seed, int mode, int64_t row_begin, int64_t n,
                             void* emb, int64_t emb_row_offset, uint64_t* attrs, int64_t attr_stride_rows,
                             bool attrs_soa, cudaStream_t st);
+
+// batched tcgen05 path (scan_tc.cu)
+struct TcParams {
+  CUtensorMap tmx;   // items: [cap_pad][ROWB] bytes, box {SW, 128}
+  CUtensorMap tmq;   // queries: [nvec][ROWB] bytes, box {SW, NP}
+  const uint64_t* attr;
+  int64_t cap_pad;
+  const uint32_t* live;
+  const DevHeader* hdr;
+  uint32_t row0;
+  int nu, V, nvec, K;
+  uint32_t wmask;
+  const KClause* cl;     // [nu][16]
+  const int* ncl;        // [nu]
+  const uint64_t* thr;   // [nu] (main pass) ; null in the sample pass (T = 0)
+  uint64_t* buf;         // [nu][cap]
+  int cap;
+  int* cnt;              // [nu]
+  int sample_tiles;      // sample pass: tiles per CTA (0 = main pass, all tiles)
+};
+
+bool tc_supported(int dtype, int dim, int nvec);
+int tc_np(int nvec);
+size_t tc_smem_bytes(int dtype, int dim, int np, int nu);
+bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes, int box_rows);
+cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st);
+cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int nu, int K, int sample_items,
+                                const DevHeader* hdr, uint64_t* thr, int* mcnt, cudaStream_t st);
+cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, const uint64_t* thr, int nu, int K,
+                               int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags, cudaStream_t st);
+cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
+                            const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
+                            cudaStream_t st);
+constexpr int kTcSampleTiles = 2;
+constexpr int kTcSampleCap = 40960;
+constexpr int kTcMainCap = 65536;
+
 
 void set_error(const std::string& msg);
 unsigned long long* debug_buffer();

@@ -1,0 +1,571 @@
+// Batched filtered top-K on the 5th-generation tensor cores (tcgen05), for query batches that make
+// scoring a real GEMM (B*V >= 16 query vectors): BASELINE.json north_star "tcgen05 tensor-core
+// tiles (kind::f16 and kind::i8) only when the query batch makes scoring a real GEMM".
+//
+// Per search (all launches on the caller's stream, no host synchronisation on the common path):
+//   1. tc_scan_kernel<SAMPLE>: a few 128-item tiles per CTA, evenly spread over the index; every
+//      passing (user, item) key is appended to the user's sample buffer.
+//   2. tc_threshold_kernel: per user, T_u = a key with exactly r sample keys >= T_u, where r is the
+//      sample count expected above the answer's K-th key plus a 6-sigma margin; T_u = 0 if the
+//      sample holds fewer than r keys (no filtering).
+//   3. tc_scan_kernel<MAIN>: every tile. Warp-specialised persistent CTA: warp 0 issues TMA loads
+//      (128-row item tile, 128B-swizzled, + the tile's attribute words and liveness bits) into a
+//      2-stage shared-memory ring; warp 1 issues tcgen05.mma (M=128 items x N=NP query vectors,
+//      K=16 bf16/f16 or 32 int8 per instruction) into a double-buffered TMEM accumulator (fp32 or
+//      exact s32); warps 4-7 (one TMEM lane = one item row per thread) tcgen05.ld the scores,
+//      max-merge each user's V columns, compare against T_u first (cheap), evaluate the user's
+//      clauses only for the rare survivors (P:4266 semantics) and append survivors' keys.
+//   4. tc_finalize_kernel: per user, the K largest appended keys, sorted, decoded; a flag marks
+//      users whose result cannot be certified (buffer overflow, or T_u > 0 with fewer than K keys
+//      appended): the host re-runs those users through the exact GEMV path.
+// Exactness: every key >= T_u is appended; if at least K are, the K-th is >= T_u, so the top-K
+// of the buffer is the top-K of the user's passing items (reading R13-style argument).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace linr {
+
+constexpr int kTcThreads = 256;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
+constexpr int kTcStages = 2;
+constexpr int kTcRows = 128;
+
+// ------------------------------------------------------------------ PTX helpers
+LINR_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+LINR_DEV void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+LINR_DEV void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+LINR_DEV void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+LINR_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+LINR_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+LINR_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+LINR_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+LINR_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+LINR_DEV void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+template <int DT>
+LINR_DEV void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (DT == LINR_I8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+LINR_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major shared-memory matrix descriptor (canonical layout: rows of SW bytes, 8-row core groups
+// SBO = 8*SW bytes apart, SW-byte swizzle; SM100 descriptor version 1).
+template <int SW>
+LINR_DEV uint64_t umma_desc(uint32_t saddr) {
+  constexpr uint64_t layout = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                          // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(((8 * SW) >> 4) & 0x3FFF) << 32;  // SBO
+  d |= (uint64_t)1 << 46;                          // version
+  d |= layout << 61;
+  return d;
+}
+
+template <int DT, int NP>
+constexpr uint32_t tc_idesc() {
+  // c_format [4,6): 1 = F32, 2 = S32; a/b format [7,10)/[10,13): F16 0, BF16 1, S8 signed 1;
+  // K-major A and B; n_dim [17,23) = N >> 3; m_dim [24,29) = M >> 4
+  uint32_t d = 0;
+  if (DT == LINR_I8) {
+    d |= 2u << 4;
+    d |= 1u << 7;
+    d |= 1u << 10;
+  } else {
+    d |= 1u << 4;
+    const uint32_t f = (DT == LINR_BF16) ? 1u : 0u;
+    d |= f << 7;
+    d |= f << 10;
+  }
+  d |= (uint32_t)(NP >> 3) << 17;
+  d |= (uint32_t)(kTcRows >> 4) << 24;
+  return d;
+}
+
+template <int DT, int D>
+struct TcGeom {
+  static constexpr int ESZ = DT == LINR_I8 ? 1 : 2;
+  static constexpr int ROWB = D * ESZ;
+  static constexpr int SW = ROWB >= 128 ? 128 : ROWB;   // swizzle span = box inner bytes
+  static constexpr int NATOM = ROWB / SW;                // swizzle atoms along K
+  static constexpr int KSTEP_B = 32;                     // bytes of K per MMA (16 x 2B or 32 x 1B)
+  static constexpr int KPA = SW / KSTEP_B;               // MMAs per atom
+  static constexpr int NKS = ROWB / KSTEP_B;
+  static constexpr int XBYTES = kTcRows * ROWB;
+};
+
+struct TcSmemCtl {
+  uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2], qbar;
+  uint32_t tmem_base;
+};
+
+template <int DT, int D, int NP>
+struct TcLayout {
+  using G = TcGeom<DT, D>;
+  static constexpr size_t q_off = 0;                                   // NATOM x [NP][SW]
+  static constexpr size_t x_off = q_off + (size_t)NP * G::ROWB;        // stages x NATOM x [128][SW]
+  static constexpr size_t a_off = x_off + (size_t)kTcStages * G::XBYTES;   // stages x (4 words x 1 KB + 16 B)
+  static constexpr size_t a_stage = 4 * 1024 + 128;
+  static constexpr size_t thr_off = a_off + kTcStages * a_stage;       // [nu] u64 thresholds
+  static constexpr size_t ctl_off(int nu) { return thr_off + ((size_t)nu * 8 + 127) / 128 * 128; }
+  static size_t bytes(int nu) { return ctl_off(nu) + sizeof(TcSmemCtl) + 1024; }   // + alignment slack
+};
+
+template <int DT, int D, int NP>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_constant__ TcParams p) {
+  using G = TcGeom<DT, D>;
+  using Lay = TcLayout<DT, D, NP>;
+  constexpr bool kInt = DT == LINR_I8;
+  extern __shared__ unsigned char smem_raw_tc[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw_tc + 1023) & ~(uintptr_t)1023);
+  unsigned char* sQ = smem + Lay::q_off;
+  unsigned char* sX = smem + Lay::x_off;
+  unsigned char* sA = smem + Lay::a_off;
+  uint64_t* sThr = reinterpret_cast<uint64_t*>(smem + Lay::thr_off);
+  TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + Lay::ctl_off(p.nu));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
+  const int64_t ntiles = (hwm + kTcRows - 1) / kTcRows;
+  // tile sequence of this CTA: the sample pass takes sample_tiles distinct tiles per CTA spread
+  // evenly over the index (every tile once if the index is smaller); the main pass strides.
+  const bool sample = p.sample_tiles > 0;
+  const int64_t stotal = (int64_t)gridDim.x * p.sample_tiles;
+  int64_t nmine;
+  if (sample) {
+    if (ntiles > stotal) nmine = p.sample_tiles;
+    else nmine = max((int64_t)0, min((int64_t)p.sample_tiles, ntiles - (int64_t)blockIdx.x * p.sample_tiles));
+  } else {
+    nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  }
+  auto tile_of = [&](int64_t i) -> int64_t {
+    if (sample) {
+      const int64_t j = (int64_t)blockIdx.x * p.sample_tiles + i;
+      return ntiles > stotal ? (j * ntiles) / stotal : j;   // distinct, evenly spread
+    }
+    return blockIdx.x + i * gridDim.x;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&ctl->full[s], 1);
+      mbar_init(&ctl->empty[s], 2);   // MMA commit + epilogue release
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&ctl->tfull[a], 1);
+      mbar_init(&ctl->tempty[a], 128);
+    }
+    mbar_init(&ctl->qbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int u = tid; u < p.nu; u += kTcThreads) sThr[u] = p.thr ? p.thr[u] : 0ull;
+  constexpr uint32_t kCols = (2 * NP) <= 32 ? 32 : ((2 * NP) <= 64 ? 64 : ((2 * NP) <= 128 ? 128 : ((2 * NP) <= 256 ? 256 : 512)));
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&ctl->tmem_base)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0 && nmine > 0) {
+      // queries once: NATOM boxes of [NP rows x SW bytes]
+      mbar_expect_tx(&ctl->qbar, (uint32_t)(NP * G::ROWB));
+      for (int a = 0; a < G::NATOM; ++a) tma_load_2d(sQ + (size_t)a * NP * G::SW, &p.tmq, a * G::SW, 0, &ctl->qbar);
+      for (int64_t i = 0; i < nmine; ++i) {
+        const int64_t t = tile_of(i);
+        const int s = (int)(i % kTcStages);
+        const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
+        mbar_wait(&ctl->empty[s], ph ^ 1u);
+        unsigned char* xs = sX + (size_t)s * G::XBYTES;
+        unsigned char* as = sA + (size_t)s * Lay::a_stage;
+        uint32_t bytes = (uint32_t)G::XBYTES + 16u;
+        for (int w = 0; w < 4; ++w)
+          if ((p.wmask >> w) & 1u) bytes += 1024u;
+        mbar_expect_tx(&ctl->full[s], bytes);
+        for (int a = 0; a < G::NATOM; ++a)
+          tma_load_2d(xs + (size_t)a * kTcRows * G::SW, &p.tmx, a * G::SW, (int)(t * kTcRows), &ctl->full[s]);
+        for (int w = 0; w < 4; ++w)
+          if ((p.wmask >> w) & 1u)
+            bulk_load(as + w * 1024, p.attr + (size_t)w * p.cap_pad + t * kTcRows, 1024u, &ctl->full[s]);
+        bulk_load(as + 4 * 1024, p.live + t * (kTcRows / 32), 16u, &ctl->full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nmine > 0) {
+      constexpr uint32_t idesc = tc_idesc<DT, NP>();
+      mbar_wait(&ctl->qbar, 0);
+      tc_fence_after();
+      const uint32_t q_s = smem_u32(sQ);
+      for (int64_t i = 0; i < nmine; ++i) {
+        const int s = (int)(i % kTcStages);
+        const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
+        const int acc = (int)(i & 1);
+        const uint32_t aph = (uint32_t)((i >> 1) & 1);
+        mbar_wait(&ctl->tempty[acc], aph ^ 1u);
+        mbar_wait(&ctl->full[s], ph);
+        tc_fence_after();
+        const uint32_t x_s = smem_u32(sX + (size_t)s * G::XBYTES);
+#pragma unroll
+        for (int k = 0; k < G::NKS; ++k) {
+          const int atom = k / G::KPA, kk = k % G::KPA;
+          const uint64_t da = umma_desc<G::SW>(x_s + (uint32_t)(atom * kTcRows * G::SW + kk * G::KSTEP_B));
+          const uint64_t db = umma_desc<G::SW>(q_s + (uint32_t)(atom * NP * G::SW + kk * G::KSTEP_B));
+          tc_mma<DT>(tmem + (uint32_t)(acc * NP), da, db, idesc, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&ctl->empty[s]);    // smem stage reusable once the MMAs have read it
+        tc_commit(&ctl->tfull[acc]);  // accumulator ready
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: thread <-> TMEM lane (item row) (warp % 4) * 32 + lane
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    for (int64_t i = 0; i < nmine; ++i) {
+      const int64_t t = tile_of(i);
+      const int s = (int)(i % kTcStages);
+      const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
+      const int acc = (int)(i & 1);
+      const uint32_t aph = (uint32_t)((i >> 1) & 1);
+      mbar_wait(&ctl->tfull[acc], aph);
+      mbar_wait(&ctl->full[s], ph);   // attribute words / live bits of this stage are visible
+      tc_fence_after();
+      const unsigned char* as = sA + (size_t)s * Lay::a_stage;
+      const uint32_t lw = reinterpret_cast<const uint32_t*>(as + 4 * 1024)[row >> 5];
+      const bool live = ((lw >> (row & 31)) & 1u) && (t * kTcRows + row < hwm);
+      const uint32_t gid = p.row0 + (uint32_t)(t * kTcRows + row);
+      float m = -INFINITY;
+      for (int c0 = 0; c0 < p.nvec; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)(acc * NP + c0), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = c0 + j;
+          if (col >= p.nvec) break;
+          const float sc = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
+          m = fmaxf(m, sc);
+          if ((col + 1) % p.V == 0) {
+            const int u = col / p.V;
+            // threshold first (cheap), clauses only for the survivors
+            bool cand = false;
+            uint64_t key = 0ull;
+            if (live) {
+              const uint64_t T = sThr[u];
+              const uint32_t hi = ordered_u32(m);
+              if (hi >= (uint32_t)(T >> 32)) {
+                key = make_key(m, gid);
+                if (key >= T) {
+                  cand = true;
+                  const int nc = p.ncl[u];
+                  for (int c = 0; c < nc && cand; ++c) {
+                    const KClause k = p.cl[u * 16 + c];
+                    const uint64_t aw = reinterpret_cast<const uint64_t*>(as + k.word * 1024)[row];
+                    const bool hit = (aw & k.mask) != 0ull;
+                    if (hit == (k.rev != 0)) cand = false;
+                  }
+                }
+              }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+            if (bal) {
+              const int leader = __ffs(bal) - 1;
+              int pos0 = 0;
+              if (lane == leader) pos0 = atomicAdd(&p.cnt[u], __popc(bal));
+              pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+              if (cand) {
+                const int pos = pos0 + __popc(bal & lanemask_lt());
+                if (pos < p.cap) p.buf[(size_t)u * p.cap + pos] = key;
+              }
+            }
+            m = -INFINITY;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&ctl->tempty[acc]);
+      // release the smem stage (the epilogue is the second of two arrivals; one per CTA)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 4 && lane == 0) mbar_arrive(&ctl->empty[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ thresholds from the sample
+__global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sbuf, const int* scnt, int scap,
+                                                              int nu, int K, int sample_items, const DevHeader* hdr,
+                                                              uint64_t* thr, int* mcnt) {
+  __shared__ SelScratch sc;
+  const int u = blockIdx.x;
+  const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&hdr->hwm);
+  const double frac = hwm > 0 ? (double)sample_items / (double)hwm : 1.0;
+  const double lam = (double)K * (frac < 1.0 ? frac : 1.0);
+  const int r = (int)ceil(lam + 6.0 * sqrt(lam) + 3.0);
+  const int n = min(scnt[u], scap);
+  uint64_t T = 0ull;
+  if (n >= r && scnt[u] <= scap) {
+    const uint64_t* b = sbuf + (size_t)u * scap;
+    T = block_select_ge<512>([b](int i) { return b[i]; }, n, r, &sc);
+  }
+  if (threadIdx.x == 0) {
+    thr[u] = T;
+    mcnt[u] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ per-user finalisation
+constexpr int kFinCap = 16384;
+struct FinSmem {
+  SelScratch sel;
+  BucketScratch bs;
+  int cnt;
+};
+__global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap,
+                                                             const uint64_t* thr, int K, int64_t* out_ids,
+                                                             float* out_scores, uint64_t* out_keys, int* flags) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
+  uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
+  uint64_t* s2 = s + kFinCap;   // 4096 keys
+  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int total = cnt[u];
+  const bool overflow = total > cap;
+  int n = min(total, cap);
+  const uint64_t* b = buf + (size_t)u * cap;
+  uint64_t T = 0ull;
+  if (n > K) T = block_select_ge<512>([b](int i) { return b[i]; }, n, K, &f->sel);
+  if (tid == 0) f->cnt = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += 512) {
+    const int i = i0 + tid;
+    const uint64_t v = i < n ? b[i] : 0ull;
+    const bool keep = i < n && v >= T;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    int at = 0;
+    if (lane == 0 && bal) at = atomicAdd(&f->cnt, __popc(bal));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (keep) s2[at + __popc(bal & lanemask_lt())] = v;
+  }
+  __syncthreads();
+  n = f->cnt;   // min(K, n) keys
+  const uint64_t* sorted = s;
+  if (!block_bucket_sort_desc<512>(s2, n, s, &f->bs)) {
+    const int P2 = next_pow2(n > 64 ? n : 64);
+    for (int i = n + tid; i < P2; i += 512) s2[i] = 0ull;
+    __syncthreads();
+    block_sort_desc<512>(s2, P2);
+    sorted = s2;
+  }
+  for (int j = tid; j < K; j += 512) {
+    const int64_t at = (int64_t)u * K + j;
+    if (out_keys) {
+      out_keys[at] = j < n ? sorted[j] : 0ull;
+    } else if (j < n) {
+      out_ids[at] = key_id(sorted[j]);
+      out_scores[at] = key_score(sorted[j]);
+    } else {
+      out_ids[at] = -1;
+      out_scores[at] = -INFINITY;
+    }
+  }
+  if (tid == 0) flags[u] = (overflow || (thr[u] != 0ull && n < K)) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ pass counts (batched path, on request)
+// One warp per 32-item group: per user, ballot of the clause predicates, popc, warp total.
+__global__ void __launch_bounds__(256) tc_count_kernel(const uint64_t* attr, int64_t cap_pad, const uint32_t* live,
+                                                       const DevHeader* hdr, const KClause* cl, const int* ncl,
+                                                       int nu, unsigned long long* counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&hdr->hwm);
+  const int64_t ngroups = (hwm + 31) / 32;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int u = 0; u < nu; ++u) {
+    unsigned long long tot = 0;
+    for (int64_t g = gw; g < ngroups; g += nw) {
+      const int64_t i = g * 32 + lane;
+      bool ok = (live[g] >> lane) & 1u;
+      for (int c = 0; c < ncl[u] && ok; ++c) {
+        const KClause k = cl[u * 16 + c];
+        const bool hit = (attr[(size_t)k.word * cap_pad + i] & k.mask) != 0ull;
+        if (hit == (k.rev != 0)) ok = false;
+      }
+      tot += __popc(__ballot_sync(0xffffffffu, ok));
+    }
+    if (lane == 0 && tot) atomicAdd(&counts[u], tot);
+  }
+}
+
+cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
+                            const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
+                            cudaStream_t st) {
+  tc_count_kernel<<<grid, 256, 0, st>>>(attr, cap_pad, live, hdr, cl, ncl, nu, counts);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const int sw = rowbytes >= 128 ? 128 : rowbytes;
+  cuuint64_t dims[2] = {(cuuint64_t)rowbytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)rowbytes};
+  cuuint32_t box[2] = {(cuuint32_t)sw, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUtensorMapSwizzle swz = sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int DT, int D, int NP>
+static cudaError_t launch_tc_np(const TcParams& p, int grid, cudaStream_t st) {
+  using Lay = TcLayout<DT, D, NP>;
+  const size_t smem = Lay::bytes(p.nu);
+  auto k = tc_scan_kernel<DT, D, NP>;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  k<<<grid, kTcThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int D>
+static cudaError_t launch_tc_d(int np, const TcParams& p, int grid, cudaStream_t st) {
+  switch (np) {
+    case 16: return launch_tc_np<DT, D, 16>(p, grid, st);
+    case 32: return launch_tc_np<DT, D, 32>(p, grid, st);
+    case 64: return launch_tc_np<DT, D, 64>(p, grid, st);
+    case 128: return launch_tc_np<DT, D, 128>(p, grid, st);
+    case 256: return launch_tc_np<DT, D, 256>(p, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool tc_supported(int dtype, int dim, int nvec) {
+  if (nvec < 1 || nvec > 256) return false;
+  if (dtype == LINR_BF16 || dtype == LINR_F16) return dim == 64 || dim == 128;
+  if (dtype == LINR_I8) return dim == 64 || dim == 128;
+  return false;
+}
+int tc_np(int nvec) {
+  int np = 16;
+  while (np < nvec) np <<= 1;
+  return np;
+}
+size_t tc_smem_bytes(int dtype, int dim, int np, int nu) {
+  const int esz = dtype == LINR_I8 ? 1 : 2;
+  const int rowb = dim * esz;
+  return (size_t)np * rowb + (size_t)kTcStages * kTcRows * rowb + kTcStages * (4 * 1024 + 128) +
+         ((size_t)nu * 8 + 127) / 128 * 128 + sizeof(TcSmemCtl) + 1024;
+}
+
+cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st) {
+  if (dtype == LINR_BF16) return dim == 128 ? launch_tc_d<LINR_BF16, 128>(np, p, grid, st)
+                                            : launch_tc_d<LINR_BF16, 64>(np, p, grid, st);
+  if (dtype == LINR_F16) return dim == 128 ? launch_tc_d<LINR_F16, 128>(np, p, grid, st)
+                                           : launch_tc_d<LINR_F16, 64>(np, p, grid, st);
+  if (dtype == LINR_I8) return dim == 128 ? launch_tc_d<LINR_I8, 128>(np, p, grid, st)
+                                          : launch_tc_d<LINR_I8, 64>(np, p, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int nu, int K, int sample_items,
+                                const DevHeader* hdr, uint64_t* thr, int* mcnt, cudaStream_t st) {
+  tc_threshold_kernel<<<nu, 512, 0, st>>>(sbuf, scnt, scap, nu, K, sample_items, hdr, thr, mcnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, const uint64_t* thr, int nu, int K,
+                               int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags, cudaStream_t st) {
+  const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kFinCap + 4096) * 8;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, thr, K, out_ids, out_scores, out_keys, flags);
+  return cudaGetLastError();
+}
+
+}  // namespace linr

@@ -225,3 +225,28 @@ def test_invalid_arguments_raise():
     with pytest.raises(LinrError):
         ix.load(torch.zeros((10, 64), dtype=torch.int8, device=DEV),
                 torch.zeros((10, 1), dtype=torch.int64, device=DEV), row0=995)   # ERANGE
+
+
+# ---------------------------------------------------------------- batched tcgen05 path (B*V >= 16)
+@pytest.mark.parametrize("dtype,d,B,V,K,preset,n", [
+    (dg.BF16, 128, 32, 1, 100, "HIGH", 100_000),
+    (dg.BF16, 128, 17, 1, 1000, "ALL", 60_000),
+    (dg.F16, 128, 64, 1, 50, "HIGH4", 40_000),
+    (dg.I8, 128, 16, 1, 1000, "LOW", 300_000),
+    (dg.I8, 64, 256, 1, 20, "HIGH", 30_000),
+    (dg.BF16, 64, 4, 8, 300, "HIGH", 80_000),
+    (dg.BF16, 128, 256, 1, 1000, "HIGH", 200_000),
+])
+def test_batched_tensor_core_path(dtype, d, B, V, K, preset, n):
+    mode = dg.MODE_DENSE if dtype == dg.I8 else dg.MODE_GRID
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    prof = ix.profile_read()
+    assert prof["launches"] == 5, prof   # sample, threshold, main, finalize, pass count: the tcgen05 path ran
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what=f"tc dt{dtype} d{d} B{B} V{V}")

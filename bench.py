@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--preset", default=PRESET)
     ap.add_argument("--items", type=int, default=N_ITEMS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pass-counts", action="store_true", help="batched path: also compute per-query pass counts")
     return ap.parse_args()
 
 
@@ -221,12 +222,14 @@ def run_gpu(args):
     def step():
         if sidx is not None:
             return sidx.search(qd, cls, K)
-        return ix.search(qd, cls, K, out=(ids, sc, ps))
+        return ix.search(qd, cls, K, out=(ids, sc, ps), want_pass=args.batch <= 8 or args.pass_counts)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    pass_count = int(step()[2][0].item())
+    r0 = ix.search(qd, cls, K)   # with pass counts (for the roofline's algorithmic bytes)
+    torch.cuda.synchronize()
+    pass_count = int(r0[2][0].item())
 
     # ---------------- device-timed region
     stream = torch.cuda.current_stream(dev)
@@ -299,6 +302,29 @@ def run_gpu(args):
                 "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                 "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
+    if args.batch > 8 and scan_ms > 0:
+        # batched path: dense stream of every row (all of them pass for some query) + the GEMM
+        import json as _json
+        pk = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        tflops_peak = pk.get("bf16_tflops_sustained", 1400.0)
+        hbm_bytes = n_local * (rowbytes + 8 + 1 / 8)
+        flops = 2.0 * args.batch * n_local * DIM
+        hbm_ach = hbm_bytes / (scan_ms / 1e3) / 1e9
+        tc_ach = flops / (scan_ms / 1e3) / 1e12
+        hf, tf = hbm_ach / peak, tc_ach / tflops_peak
+        common = {"kernel": "tc_scan_kernel<bf16,128,NP> (sample + thresholds + main pass)",
+                  "scan_ms_per_launch": round(scan_ms, 5),
+                  "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
+                  "hbm_frac": round(hf, 4), "tensor_frac": round(tf, 4),
+                  "alg_bytes_per_launch": int(hbm_bytes), "alg_flops_per_launch": int(flops)}
+        if tf >= hf:
+            roof = {"bound": "tensor", "achieved": round(tc_ach, 1), "peak": tflops_peak, "unit": "TFLOP/s",
+                    "frac": round(tf, 4), "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)", **common}
+        else:
+            roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": peak, "unit": "GB/s", "frac": round(hf, 4),
+                    "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common}
     launches_per_step = prof["launches"] / max(1, prof["searches"])
     if world > 1:
         launches_per_step += 1   # merge kernel after the all-gather

@@ -186,7 +186,7 @@ struct TcWs {
   size_t sbuf, scnt, thr, mbuf, mcnt, flags, cl, ncl, gemv, end;
 };
 bool use_tc(const linr_index* ix, int B, int V) {
-  return B * V >= 16 && tc_supported(ix->d.dtype, ix->d.dim, B * V) &&
+  return B * V >= 16 && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B) <= ix->smem_optin;
 }
 bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
@@ -194,11 +194,12 @@ bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* 
   if (!make_plan(ix, 1, V, K, &g, why)) return false;   // exact GEMV fallback for uncertified users
   const size_t nu = (size_t)B;
   w->sbuf = 0;
-  w->scnt = align256(w->sbuf + nu * kTcSampleCap * 8);
-  w->thr = align256(w->scnt + nu * 4);
+  const size_t G = (size_t)ix->num_sms;
+  w->scnt = align256(w->sbuf + nu * G * kTcSampleCap * 8);
+  w->thr = align256(w->scnt + nu * G * 4);
   w->mbuf = align256(w->thr + nu * 8);
-  w->mcnt = align256(w->mbuf + nu * kTcMainCap * 8);
-  w->flags = align256(w->mcnt + nu * 4);
+  w->mcnt = align256(w->mbuf + nu * G * kTcMainCap * 8);
+  w->flags = align256(w->mcnt + nu * G * 4);
   w->cl = align256(w->flags + nu * 4);
   w->ncl = align256(w->cl + nu * 16 * sizeof(KClause));
   w->gemv = align256(w->ncl + nu * 4);
@@ -263,7 +264,6 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   e = cudaMemcpyAsync(W + w.cl, hcl, clb, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(W + w.ncl, hncl, nclb, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaEventRecord(ix->pin_ev, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(W + w.scnt, 0, (size_t)B * 4, st);
   if (e != cudaSuccess) return cuda_fail(e, "batched staging");
 
   ProfEvents pe{};
@@ -290,6 +290,7 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   p.wmask = wmask;
   p.cl = (const KClause*)(W + w.cl);
   p.ncl = (const int*)(W + w.ncl);
+  p.dbg = nullptr;
   // 1. sample pass (no threshold)
   p.thr = nullptr;
   p.buf = (uint64_t*)(W + w.sbuf);
@@ -299,8 +300,8 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p, ix->num_sms, st);
   if (e != cudaSuccess) return cuda_fail(e, "tc sample launch");
   // 2. thresholds
-  e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, B, K,
-                          ix->num_sms * kTcSampleTiles * 128, ix->hdr, (uint64_t*)(W + w.thr), (int*)(W + w.mcnt), st);
+  e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, ix->num_sms, B, K,
+                          ix->num_sms * kTcSampleTiles * 128, ix->hdr, (uint64_t*)(W + w.thr), st);
   if (e != cudaSuccess) return cuda_fail(e, "tc threshold launch");
   // 3. main pass
   p.thr = (const uint64_t*)(W + w.thr);
@@ -308,11 +309,12 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   p.cap = kTcMainCap;
   p.cnt = (int*)(W + w.mcnt);
   p.sample_tiles = 0;
+  p.dbg = debug_buffer();
   e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p, ix->num_sms, st);
   if (e != cudaSuccess) return cuda_fail(e, "tc main launch");
   if (ix->prof) cudaEventRecord(pe.e1, st);
   // 4. finalize
-  e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), kTcMainCap,
+  e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), kTcMainCap, ix->num_sms,
                          (const uint64_t*)(W + w.thr), B, K, mode == 0 ? out_ids : nullptr,
                          mode == 0 ? out_scores : nullptr, mode == 1 ? out_keys : nullptr, (int*)(W + w.flags), st);
   if (e != cudaSuccess) return cuda_fail(e, "tc finalize launch");

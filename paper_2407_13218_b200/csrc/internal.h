@@ -119,27 +119,29 @@ struct TcParams {
   const KClause* cl;     // [nu][16]
   const int* ncl;        // [nu]
   const uint64_t* thr;   // [nu] (main pass) ; null in the sample pass (T = 0)
-  uint64_t* buf;         // [nu][cap]
+  uint64_t* buf;         // [nu][grid][cap] per-(user, CTA) regions
   int cap;
-  int* cnt;              // [nu]
+  int* cnt;              // [nu][grid] keys each CTA produced for each user (may exceed cap)
   int sample_tiles;      // sample pass: tiles per CTA (0 = main pass, all tiles)
+  unsigned long long* dbg;   // diagnostics: per-tile role timestamps of CTA 0 (null = off)
 };
 
-bool tc_supported(int dtype, int dim, int nvec);
+bool tc_supported(int dtype, int dim, int nvec, int V);
 int tc_np(int nvec);
 size_t tc_smem_bytes(int dtype, int dim, int np, int nu);
 bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes, int box_rows);
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st);
-cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int nu, int K, int sample_items,
-                                const DevHeader* hdr, uint64_t* thr, int* mcnt, cudaStream_t st);
-cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, const uint64_t* thr, int nu, int K,
-                               int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags, cudaStream_t st);
+cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
+                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st);
+cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
+                               int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
+                               cudaStream_t st);
 cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
                             const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
                             cudaStream_t st);
 constexpr int kTcSampleTiles = 2;
-constexpr int kTcSampleCap = 40960;
-constexpr int kTcMainCap = 65536;
+constexpr int kTcSampleCap = kTcSampleTiles * 128;   // per (user, CTA) region: cannot overflow
+constexpr int kTcMainCap = 256;                      // per (user, CTA) region of the main pass
 
 
 void set_error(const std::string& msg);

@@ -29,8 +29,10 @@
 
 namespace linr {
 
-constexpr int kTcThreads = 256;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
-constexpr int kTcStages = 2;
+constexpr int kTcThreads = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
+constexpr int kTcXStagesMax = 4;  // item-tile ring (released by the MMA commit); 3 when the queries are large
+constexpr int tc_xstages(int np, int rowb) { return (size_t)np * rowb + (size_t)4 * 128 * rowb > 160 * 1024 ? 3 : 4; }
+constexpr int kTcAStages = 4;     // attribute ring (released by the epilogue)
 constexpr int kTcRows = 128;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -47,7 +49,7 @@ LINR_DEV void mbar_arrive(uint64_t* b) {
 LINR_DEV void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 2000;\n\t"
       "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
@@ -86,6 +88,17 @@ LINR_DEV void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, 
         "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
         : "memory");
   }
+}
+LINR_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 LINR_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
@@ -143,19 +156,25 @@ struct TcGeom {
 };
 
 struct TcSmemCtl {
-  uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2], qbar;
+  uint64_t xfull[kTcXStagesMax], xempty[kTcXStagesMax], afull[kTcAStages], aempty[kTcAStages];
+  uint64_t tfull[2], tempty[2], qbar;
   uint32_t tmem_base;
 };
 
 template <int DT, int D, int NP>
 struct TcLayout {
   using G = TcGeom<DT, D>;
-  static constexpr size_t q_off = 0;                                   // NATOM x [NP][SW]
-  static constexpr size_t x_off = q_off + (size_t)NP * G::ROWB;        // stages x NATOM x [128][SW]
-  static constexpr size_t a_off = x_off + (size_t)kTcStages * G::XBYTES;   // stages x (4 words x 1 KB + 16 B)
+  static constexpr size_t q_off = 0;                                        // NATOM x [NP][SW]
+  static constexpr size_t x_off = q_off + (size_t)NP * G::ROWB;             // XS x NATOM x [128][SW]
+  static constexpr int XS = tc_xstages(NP, G::ROWB);
+  static constexpr size_t a_off = x_off + (size_t)XS * G::XBYTES;   // AS x (4 words x 1 KB + 16 B)
   static constexpr size_t a_stage = 4 * 1024 + 128;
-  static constexpr size_t thr_off = a_off + kTcStages * a_stage;       // [nu] u64 thresholds
-  static constexpr size_t ctl_off(int nu) { return thr_off + ((size_t)nu * 8 + 127) / 128 * 128; }
+  static constexpr size_t thr_off = a_off + kTcAStages * a_stage;           // [nu] u64 keys, [nu] f32 scores
+  static constexpr size_t thrf_off(int nu) { return thr_off + ((size_t)nu * 8 + 15) / 16 * 16; }
+  static constexpr size_t scr_off(int nu) { return (thrf_off(nu) + (size_t)(nu + 31) / 32 * 32 * 4 + 127) / 128 * 128; }
+  static constexpr size_t scr_bytes = (size_t)(kTcThreads / 32 - 4) * 32 * 33 * 4;
+  static constexpr size_t cnt_off(int nu) { return scr_off(nu) + scr_bytes; }
+  static constexpr size_t ctl_off(int nu) { return cnt_off(nu) + ((size_t)nu * 4 + 15) / 16 * 16; }
   static size_t bytes(int nu) { return ctl_off(nu) + sizeof(TcSmemCtl) + 1024; }   // + alignment slack
 };
 
@@ -164,13 +183,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   using G = TcGeom<DT, D>;
   using Lay = TcLayout<DT, D, NP>;
   constexpr bool kInt = DT == LINR_I8;
-  extern __shared__ unsigned char smem_raw_tc[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw_tc + 1023) & ~(uintptr_t)1023);
+  constexpr int NEPI = kTcThreads - 128;   // epilogue threads (warps 4..)
+  extern __shared__ __align__(1024) unsigned char smem_raw_tc[];
+  // 1024-byte alignment for the 128B-swizzled TMA/UMMA tiles; indexing the extern array keeps the
+  // pointers in the shared window (LDS/STS rather than generic loads)
+  unsigned char* smem = smem_raw_tc + ((1024u - (smem_u32(smem_raw_tc) & 1023u)) & 1023u);
   unsigned char* sQ = smem + Lay::q_off;
   unsigned char* sX = smem + Lay::x_off;
   unsigned char* sA = smem + Lay::a_off;
   uint64_t* sThr = reinterpret_cast<uint64_t*>(smem + Lay::thr_off);
+  float* sThrF = reinterpret_cast<float*>(smem + Lay::thrf_off(p.nu));   // padded to 32 users, 16B aligned
   TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + Lay::ctl_off(p.nu));
+  float* scratch = reinterpret_cast<float*>(smem + Lay::scr_off(p.nu));
+  int* sCnt = reinterpret_cast<int*>(smem + Lay::cnt_off(p.nu));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
@@ -195,18 +220,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&ctl->full[s], 1);
-      mbar_init(&ctl->empty[s], 2);   // MMA commit + epilogue release
+    for (int s = 0; s < Lay::XS; ++s) {
+      mbar_init(&ctl->xfull[s], 1);
+      mbar_init(&ctl->xempty[s], 1);   // released by the MMA commit
+    }
+    for (int s = 0; s < kTcAStages; ++s) {
+      mbar_init(&ctl->afull[s], 1);
+      mbar_init(&ctl->aempty[s], NEPI / 32);   // released by every epilogue warp
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&ctl->tfull[a], 1);
-      mbar_init(&ctl->tempty[a], 128);
+      mbar_init(&ctl->tempty[a], NEPI);
     }
     mbar_init(&ctl->qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int u = tid; u < p.nu; u += kTcThreads) sThr[u] = p.thr ? p.thr[u] : 0ull;
+  for (int u = tid; u < p.nu; u += kTcThreads) sCnt[u] = 0;
+  for (int u = tid; u < (p.nu + 31) / 32 * 32; u += kTcThreads) {
+    if (u < p.nu) {
+      const uint64_t T = p.thr ? p.thr[u] : 0ull;
+      sThr[u] = T;
+      sThrF[u] = T ? key_score(T) : -INFINITY;   // score part of the threshold (ties: full key check)
+    } else {
+      sThrF[u] = INFINITY;                        // padding users never qualify
+    }
+  }
   constexpr uint32_t kCols = (2 * NP) <= 32 ? 32 : ((2 * NP) <= 64 ? 64 : ((2 * NP) <= 128 ? 128 : ((2 * NP) <= 256 ? 256 : 512)));
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&ctl->tmem_base)),
@@ -224,23 +262,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       // queries once: NATOM boxes of [NP rows x SW bytes]
       mbar_expect_tx(&ctl->qbar, (uint32_t)(NP * G::ROWB));
       for (int a = 0; a < G::NATOM; ++a) tma_load_2d(sQ + (size_t)a * NP * G::SW, &p.tmq, a * G::SW, 0, &ctl->qbar);
+      uint32_t abytes = 16u;
+      for (int w = 0; w < 4; ++w)
+        if ((p.wmask >> w) & 1u) abytes += 1024u;
       for (int64_t i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
-        const int s = (int)(i % kTcStages);
-        const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
-        mbar_wait(&ctl->empty[s], ph ^ 1u);
-        unsigned char* xs = sX + (size_t)s * G::XBYTES;
-        unsigned char* as = sA + (size_t)s * Lay::a_stage;
-        uint32_t bytes = (uint32_t)G::XBYTES + 16u;
-        for (int w = 0; w < 4; ++w)
-          if ((p.wmask >> w) & 1u) bytes += 1024u;
-        mbar_expect_tx(&ctl->full[s], bytes);
+        const int xs = (int)(i % Lay::XS), as = (int)(i % kTcAStages);
+        const uint32_t xph = (uint32_t)((i / Lay::XS) & 1), aph = (uint32_t)((i / kTcAStages) & 1);
+        mbar_wait(&ctl->xempty[xs], xph ^ 1u);
+        if (p.dbg && blockIdx.x == 0 && i < 64) p.dbg[i * 4 + 0] = gtimer();
+        unsigned char* xd = sX + (size_t)xs * G::XBYTES;
+        mbar_expect_tx(&ctl->xfull[xs], (uint32_t)G::XBYTES);
         for (int a = 0; a < G::NATOM; ++a)
-          tma_load_2d(xs + (size_t)a * kTcRows * G::SW, &p.tmx, a * G::SW, (int)(t * kTcRows), &ctl->full[s]);
+          tma_load_2d(xd + (size_t)a * kTcRows * G::SW, &p.tmx, a * G::SW, (int)(t * kTcRows), &ctl->xfull[xs]);
+        mbar_wait(&ctl->aempty[as], aph ^ 1u);
+        unsigned char* ad = sA + (size_t)as * Lay::a_stage;
+        mbar_expect_tx(&ctl->afull[as], abytes);
         for (int w = 0; w < 4; ++w)
           if ((p.wmask >> w) & 1u)
-            bulk_load(as + w * 1024, p.attr + (size_t)w * p.cap_pad + t * kTcRows, 1024u, &ctl->full[s]);
-        bulk_load(as + 4 * 1024, p.live + t * (kTcRows / 32), 16u, &ctl->full[s]);
+            bulk_load(ad + w * 1024, p.attr + (size_t)w * p.cap_pad + t * kTcRows, 1024u, &ctl->afull[as]);
+        bulk_load(ad + 4 * 1024, p.live + t * (kTcRows / 32), 16u, &ctl->afull[as]);
       }
     }
   } else if (warp == 1) {
@@ -250,14 +291,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       tc_fence_after();
       const uint32_t q_s = smem_u32(sQ);
       for (int64_t i = 0; i < nmine; ++i) {
-        const int s = (int)(i % kTcStages);
-        const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
+        const int xs = (int)(i % Lay::XS);
+        const uint32_t xph = (uint32_t)((i / Lay::XS) & 1);
         const int acc = (int)(i & 1);
-        const uint32_t aph = (uint32_t)((i >> 1) & 1);
-        mbar_wait(&ctl->tempty[acc], aph ^ 1u);
-        mbar_wait(&ctl->full[s], ph);
+        const uint32_t tph = (uint32_t)((i >> 1) & 1);
+        mbar_wait(&ctl->tempty[acc], tph ^ 1u);
+        mbar_wait(&ctl->xfull[xs], xph);
         tc_fence_after();
-        const uint32_t x_s = smem_u32(sX + (size_t)s * G::XBYTES);
+        if (p.dbg && blockIdx.x == 0 && i < 64) p.dbg[i * 4 + 1] = gtimer();
+        const uint32_t x_s = smem_u32(sX + (size_t)xs * G::XBYTES);
 #pragma unroll
         for (int k = 0; k < G::NKS; ++k) {
           const int atom = k / G::KPA, kk = k % G::KPA;
@@ -265,153 +307,216 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           const uint64_t db = umma_desc<G::SW>(q_s + (uint32_t)(atom * NP * G::SW + kk * G::KSTEP_B));
           tc_mma<DT>(tmem + (uint32_t)(acc * NP), da, db, idesc, k > 0 ? 1u : 0u);
         }
-        tc_commit(&ctl->empty[s]);    // smem stage reusable once the MMAs have read it
+        tc_commit(&ctl->xempty[xs]);  // item tile reusable once the MMAs have read it
         tc_commit(&ctl->tfull[acc]);  // accumulator ready
       }
     }
   } else if (warp >= 4) {
-    // ---- epilogue: thread <-> TMEM lane (item row) (warp % 4) * 32 + lane
+    // ---- epilogue: thread <-> TMEM lane (item row) (warp % 4) * 32 + lane; the two epilogue
+    // warpgroups split the accumulator columns in 32-column chunks (each chunk = 32/V users).
     const int row = (warp & 3) * 32 + lane;
+    const int grp = (warp - 4) >> 2;
+    constexpr int NGRP = NEPI / 128;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int V = p.V;                       // 1, 2, 4 or 8
+    const int lv = V == 1 ? 0 : (V == 2 ? 1 : (V == 4 ? 2 : 3));
+    const int nchunks = (p.nvec + 31) / 32;
     for (int64_t i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
-      const int s = (int)(i % kTcStages);
-      const uint32_t ph = (uint32_t)((i / kTcStages) & 1);
+      const int as = (int)(i % kTcAStages);
+      const uint32_t aph = (uint32_t)((i / kTcAStages) & 1);
       const int acc = (int)(i & 1);
-      const uint32_t aph = (uint32_t)((i >> 1) & 1);
-      mbar_wait(&ctl->tfull[acc], aph);
-      mbar_wait(&ctl->full[s], ph);   // attribute words / live bits of this stage are visible
+      const uint32_t tph = (uint32_t)((i >> 1) & 1);
+      mbar_wait(&ctl->tfull[acc], tph);
+      mbar_wait(&ctl->afull[as], aph);
       tc_fence_after();
-      const unsigned char* as = sA + (size_t)s * Lay::a_stage;
-      const uint32_t lw = reinterpret_cast<const uint32_t*>(as + 4 * 1024)[row >> 5];
+      if (p.dbg && blockIdx.x == 0 && i < 64 && tid == 128) p.dbg[i * 4 + 2] = gtimer();
+      const unsigned char* ad = sA + (size_t)as * Lay::a_stage;
+      const uint32_t lw = reinterpret_cast<const uint32_t*>(ad + 4 * 1024)[row >> 5];
       const bool live = ((lw >> (row & 31)) & 1u) && (t * kTcRows + row < hwm);
       const uint32_t gid = p.row0 + (uint32_t)(t * kTcRows + row);
-      float m = -INFINITY;
-      for (int c0 = 0; c0 < p.nvec; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + lane_base + (uint32_t)(acc * NP + c0), v);
+      for (int ch = grp; ch < nchunks; ch += NGRP) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)(acc * NP + ch * 32), v);
+        const int u0 = (ch * 32) >> lv;
+        float sc[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
-          if (col >= p.nvec) break;
-          const float sc = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
-          m = fmaxf(m, sc);
-          if ((col + 1) % p.V == 0) {
-            const int u = col / p.V;
-            // threshold first (cheap), clauses only for the survivors
-            bool cand = false;
-            uint64_t key = 0ull;
-            if (live) {
-              const uint64_t T = sThr[u];
-              const uint32_t hi = ordered_u32(m);
-              if (hi >= (uint32_t)(T >> 32)) {
-                key = make_key(m, gid);
-                if (key >= T) {
-                  cand = true;
-                  const int nc = p.ncl[u];
-                  for (int c = 0; c < nc && cand; ++c) {
-                    const KClause k = p.cl[u * 16 + c];
-                    const uint64_t aw = reinterpret_cast<const uint64_t*>(as + k.word * 1024)[row];
-                    const bool hit = (aw & k.mask) != 0ull;
-                    if (hit == (k.rev != 0)) cand = false;
-                  }
-                }
-              }
+        for (int j = 0; j < 32; ++j) sc[j] = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
+        // candidate mask: bit j = first column of a user whose max reaches the user's threshold score
+        uint32_t cm = 0;
+        if (V == 1) {
+          const float4* tf = reinterpret_cast<const float4*>(sThrF + u0);   // u0 % 32 == 0: aligned
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 t4 = tf[j4];
+            cm |= (sc[4 * j4] >= t4.x ? 1u : 0u) << (4 * j4);
+            cm |= (sc[4 * j4 + 1] >= t4.y ? 1u : 0u) << (4 * j4 + 1);
+            cm |= (sc[4 * j4 + 2] >= t4.z ? 1u : 0u) << (4 * j4 + 2);
+            cm |= (sc[4 * j4 + 3] >= t4.w ? 1u : 0u) << (4 * j4 + 3);
+          }
+        } else {
+          // max over each user's V in {2,4,8} aligned columns: butterfly inside groups of V
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) { const float m = fmaxf(sc[j], sc[j + 1]); sc[j] = m; sc[j + 1] = m; }
+          if (V >= 4) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float m0 = fmaxf(sc[j], sc[j + 2]);
+              sc[j] = m0; sc[j + 1] = m0; sc[j + 2] = m0; sc[j + 3] = m0;
             }
-            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-            if (bal) {
-              const int leader = __ffs(bal) - 1;
-              int pos0 = 0;
-              if (lane == leader) pos0 = atomicAdd(&p.cnt[u], __popc(bal));
-              pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-              if (cand) {
-                const int pos = pos0 + __popc(bal & lanemask_lt());
-                if (pos < p.cap) p.buf[(size_t)u * p.cap + pos] = key;
-              }
+          }
+          if (V >= 8) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              const float m0 = fmaxf(sc[j], sc[j + 4]);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) sc[j + k] = m0;
             }
-            m = -INFINITY;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            if ((j & (V - 1)) != 0) continue;
+            cm |= (sc[j] >= sThrF[u0 + (j >> lv)] ? 1u : 0u) << j;
           }
         }
+        if (!live) cm = 0u;
+        uint32_t wor = __reduce_or_sync(0xffffffffu, cm);
+        if (wor == 0u) continue;
+        // rare: stage this lane's scores, then visit only the users some lane flagged
+        float* scr = scratch + (size_t)(warp - 4) * 32 * 33 + lane * 33;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) scr[j] = sc[j];
+        __syncwarp();
+        while (wor) {
+          const int j = __ffs(wor) - 1;
+          wor &= wor - 1u;
+          const int u = u0 + (j >> lv);
+          const bool flagged = (cm >> j) & 1u;
+          bool cand = false;
+          uint64_t key = 0ull;
+          if (flagged) {
+            const float m = scr[j];
+            key = make_key(m, gid);
+            if (key >= sThr[u]) {
+              cand = true;
+              const int nc = __ldg(p.ncl + u);
+              for (int c = 0; c < nc && cand; ++c) {
+                const uint4 kr = __ldg(reinterpret_cast<const uint4*>(p.cl) + u * 16 + c);
+                const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
+                const uint64_t aw = reinterpret_cast<const uint64_t*>(ad + kr.z * 1024)[row];
+                const bool hit = (aw & mask) != 0ull;
+                if (hit == (kr.w != 0u)) cand = false;
+              }
+            }
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+          if (bal) {   // this CTA's region of user u: shared-memory counter, fire-and-forget stores
+            const int leader = __ffs(bal) - 1;
+            int pos0 = 0;
+            if (lane == leader) pos0 = atomicAdd(&sCnt[u], __popc(bal));
+            pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+            if (cand) {
+              const int pos = pos0 + __popc(bal & lanemask_lt());
+              if (pos < p.cap) p.buf[((size_t)u * gridDim.x + blockIdx.x) * p.cap + pos] = key;
+            }
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&ctl->tempty[acc]);
-      // release the smem stage (the epilogue is the second of two arrivals; one per CTA)
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 4 && lane == 0) mbar_arrive(&ctl->empty[s]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->aempty[as]);   // one arrival per epilogue warp
+      if (p.dbg && blockIdx.x == 0 && i < 64 && tid == 128) p.dbg[i * 4 + 3] = gtimer();
     }
   }
   tc_fence_before();
   __syncthreads();
+  for (int u = tid; u < p.nu; u += kTcThreads) p.cnt[(size_t)u * gridDim.x + blockIdx.x] = sCnt[u];
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
   }
 }
 
+// ------------------------------------------------------------------ per-user region gather
+// Keys of user u live in grid regions buf[(u*grid + c)*cap + 0..min(cnt[u*grid+c], cap)). Gather at
+// most `room` of them into dst (shared memory). Returns the number gathered; *total = all keys
+// (including any beyond the region capacity: total > gathered means an overflowed region).
+template <int NT>
+__device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int cap, int u, uint64_t* dst, int room,
+                              int* s_n, long long* s_total, long long* total) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { *s_n = 0; *s_total = 0; }
+  __syncthreads();
+  for (int c = warp; c < grid; c += NT / 32) {   // warp per region
+    const int raw = cnt[(size_t)u * grid + c];
+    const int m = min(raw, cap);
+    if (lane == 0) atomicAdd((unsigned long long*)s_total, (unsigned long long)raw);
+    int at = 0;
+    if (lane == 0 && m) at = atomicAdd(s_n, m);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    const uint64_t* r = buf + ((size_t)u * grid + c) * cap;
+    for (int j = lane; j < m; j += 32)
+      if (at + j < room) dst[at + j] = r[j];
+  }
+  __syncthreads();
+  *total = *s_total;
+  return min(*s_n, room);
+}
+
 // ------------------------------------------------------------------ thresholds from the sample
+constexpr int kTcGatherCap = 16384;
 __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sbuf, const int* scnt, int scap,
-                                                              int nu, int K, int sample_items, const DevHeader* hdr,
-                                                              uint64_t* thr, int* mcnt) {
-  __shared__ SelScratch sc;
+                                                              int grid, int nu, int K, int sample_items,
+                                                              const DevHeader* hdr, uint64_t* thr) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  SelScratch* sc = reinterpret_cast<SelScratch*>(tsm);
+  int* s_n = reinterpret_cast<int*>(sc + 1);
+  long long* s_total = reinterpret_cast<long long*>(s_n + 2);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(tsm + ((sizeof(SelScratch) + 32 + 15) & ~size_t(15)));
   const int u = blockIdx.x;
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&hdr->hwm);
   const double frac = hwm > 0 ? (double)sample_items / (double)hwm : 1.0;
   const double lam = (double)K * (frac < 1.0 ? frac : 1.0);
   const int r = (int)ceil(lam + 6.0 * sqrt(lam) + 3.0);
-  const int n = min(scnt[u], scap);
+  long long total = 0;
+  // any subset of the sample gives a valid (smaller or equal) r-th key
+  const int n = gather_regions<512>(sbuf, scnt, grid, scap, u, keys, kTcGatherCap, s_n, s_total, &total);
   uint64_t T = 0ull;
-  if (n >= r && scnt[u] <= scap) {
-    const uint64_t* b = sbuf + (size_t)u * scap;
-    T = block_select_ge<512>([b](int i) { return b[i]; }, n, r, &sc);
-  }
-  if (threadIdx.x == 0) {
-    thr[u] = T;
-    mcnt[u] = 0;
-  }
+  if (n >= r) T = block_select_ge<512>([keys](int i) { return keys[i]; }, n, r, sc);
+  if (threadIdx.x == 0) thr[u] = T;
 }
 
 // ------------------------------------------------------------------ per-user finalisation
-constexpr int kFinCap = 16384;
 struct FinSmem {
   SelScratch sel;
   BucketScratch bs;
-  int cnt;
+  int n;
+  long long total;
 };
-__global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap,
+__global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap, int grid,
                                                              const uint64_t* thr, int K, int64_t* out_ids,
                                                              float* out_scores, uint64_t* out_keys, int* flags) {
   extern __shared__ __align__(16) unsigned char fsm[];
   FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
   uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
-  uint64_t* s2 = s + kFinCap;   // 4096 keys
-  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  const int total = cnt[u];
-  const bool overflow = total > cap;
-  int n = min(total, cap);
-  const uint64_t* b = buf + (size_t)u * cap;
-  uint64_t T = 0ull;
-  if (n > K) T = block_select_ge<512>([b](int i) { return b[i]; }, n, K, &f->sel);
-  if (tid == 0) f->cnt = 0;
-  __syncthreads();
-  for (int i0 = 0; i0 < n; i0 += 512) {
-    const int i = i0 + tid;
-    const uint64_t v = i < n ? b[i] : 0ull;
-    const bool keep = i < n && v >= T;
-    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    int at = 0;
-    if (lane == 0 && bal) at = atomicAdd(&f->cnt, __popc(bal));
-    at = __shfl_sync(0xffffffffu, at, 0);
-    if (keep) s2[at + __popc(bal & lanemask_lt())] = v;
+  uint64_t* s2 = s + kTcGatherCap;   // 4096 keys
+  const int u = blockIdx.x, tid = threadIdx.x;
+  long long total = 0;
+  int n = gather_regions<512>(buf, cnt, grid, cap, u, s, kTcGatherCap, &f->n, &f->total, &total);
+  const bool overflow = total > n;   // a region overflowed or the gather room was exceeded
+  if (n > K) {
+    const uint64_t T = block_select_ge<512>([s](int i) { return s[i]; }, n, K, &f->sel);
+    n = block_compact_ge<512>(s, n, T, &f->sel);
   }
-  __syncthreads();
-  n = f->cnt;   // min(K, n) keys
-  const uint64_t* sorted = s;
-  if (!block_bucket_sort_desc<512>(s2, n, s, &f->bs)) {
+  const uint64_t* sorted = s2;
+  if (!block_bucket_sort_desc<512>(s, n, s2, &f->bs)) {
     const int P2 = next_pow2(n > 64 ? n : 64);
-    for (int i = n + tid; i < P2; i += 512) s2[i] = 0ull;
+    for (int i = n + tid; i < P2; i += 512) s[i] = 0ull;
     __syncthreads();
-    block_sort_desc<512>(s2, P2);
-    sorted = s2;
+    block_sort_desc<512>(s, P2);
+    sorted = s;
   }
   for (int j = tid; j < K; j += 512) {
     const int64_t at = (int64_t)u * K + j;
@@ -521,8 +626,9 @@ static cudaError_t launch_tc_d(int np, const TcParams& p, int grid, cudaStream_t
   return cudaErrorInvalidValue;
 }
 
-bool tc_supported(int dtype, int dim, int nvec) {
+bool tc_supported(int dtype, int dim, int nvec, int V) {
   if (nvec < 1 || nvec > 256) return false;
+  if (V != 1 && V != 2 && V != 4 && V != 8) return false;   // a user's columns stay inside a 32-column chunk
   if (dtype == LINR_BF16 || dtype == LINR_F16) return dim == 64 || dim == 128;
   if (dtype == LINR_I8) return dim == 64 || dim == 128;
   return false;
@@ -535,8 +641,9 @@ int tc_np(int nvec) {
 size_t tc_smem_bytes(int dtype, int dim, int np, int nu) {
   const int esz = dtype == LINR_I8 ? 1 : 2;
   const int rowb = dim * esz;
-  return (size_t)np * rowb + (size_t)kTcStages * kTcRows * rowb + kTcStages * (4 * 1024 + 128) +
-         ((size_t)nu * 8 + 127) / 128 * 128 + sizeof(TcSmemCtl) + 1024;
+  return (size_t)np * rowb + (size_t)tc_xstages(np, rowb) * kTcRows * rowb + kTcAStages * (4 * 1024 + 128) +
+         (size_t)nu * 8 + 16 + (size_t)(nu + 31) / 32 * 32 * 4 + 128 + (size_t)(kTcThreads / 32 - 4) * 32 * 33 * 4 +
+         (size_t)nu * 4 + 16 + sizeof(TcSmemCtl) + 1024;
 }
 
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st) {
@@ -549,22 +656,30 @@ cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int gr
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int nu, int K, int sample_items,
-                                const DevHeader* hdr, uint64_t* thr, int* mcnt, cudaStream_t st) {
-  tc_threshold_kernel<<<nu, 512, 0, st>>>(sbuf, scnt, scap, nu, K, sample_items, hdr, thr, mcnt);
+cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
+                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st) {
+  const size_t smem = ((sizeof(SelScratch) + 32 + 15) & ~size_t(15)) + (size_t)kTcGatherCap * 8;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_threshold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  tc_threshold_kernel<<<nu, 512, smem, st>>>(sbuf, scnt, scap, grid, nu, K, sample_items, hdr, thr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, const uint64_t* thr, int nu, int K,
-                               int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags, cudaStream_t st) {
-  const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kFinCap + 4096) * 8;
+cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
+                               int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
+                               cudaStream_t st) {
+  const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcGatherCap + 4096) * 8;
   static size_t set = 0;
   if (smem > set) {
     cudaError_t e = cudaFuncSetAttribute(tc_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     set = smem;
   }
-  tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, thr, K, out_ids, out_scores, out_keys, flags);
+  tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags);
   return cudaGetLastError();
 }
 

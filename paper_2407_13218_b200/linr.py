@@ -227,7 +227,7 @@ class Index:
         assert q.dtype == TORCH_DTYPE[self.dtype] and q.shape[-1] == self.dim and q.device == self.device
         return q.contiguous()
 
-    def search(self, queries: torch.Tensor, clauses, K: int, out=None):
+    def search(self, queries: torch.Tensor, clauses, K: int, out=None, want_pass: bool = True):
         """Filtered top-K. queries [B][d] or [B][V][d] (index dtype, on device); clauses: per-query
         lists of (mask, word, reverse) or a Clauses object. Returns (ids [B][K] int64,
         scores [B][K] fp32, pass [B] int64) on the device."""
@@ -243,8 +243,8 @@ class Index:
             ids, sc, ps = out
         ws = self.workspace(B, V, K)
         _check(library().linr_search(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
-                                     ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
-                                     _stream(self.device)))
+                                     ws.numel(), ids.data_ptr(), sc.data_ptr(),
+                                     ps.data_ptr() if want_pass else None, _stream(self.device)))
         return ids, sc, ps
 
     def search_keys(self, queries: torch.Tensor, clauses, K: int, out=None):

@@ -185,9 +185,19 @@ WsLayout ws_layout(const Plan& pl, int B, int K) {
 struct TcWs {
   size_t sbuf, scnt, thr, mbuf, mcnt, flags, cl, ncl, gemv, end;
 };
-bool use_tc(const linr_index* ix, int B, int V) {
+int max_clauses(const int32_t* off, int B) {
+  int m = 0;
+  for (int b = 0; b < B; ++b) m = std::max(m, (int)(off[b + 1] - off[b]));
+  return m;
+}
+int max_word(const linr_clause* cl, const int32_t* off, int B) {   // attribute words the clauses read
+  int w = 0;
+  for (int i = 0; i < off[B]; ++i) w = std::max(w, (int)cl[i].word + 1);
+  return w;
+}
+bool use_tc(const linr_index* ix, int B, int V, int maxc, int wmax) {
   return B * V >= 16 && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
-         tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B) <= ix->smem_optin;
+         tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
 }
 bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
   Plan g;
@@ -250,7 +260,6 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   int* hncl = (int*)((char*)ix->pin + clb);
   int* hflags = (int*)((char*)ix->pin + clb + nclb);
   std::memset(hcl, 0, clb);
-  uint32_t wmask = 0;
   for (int b = 0; b < B; ++b) {
     hncl[b] = off[b + 1] - off[b];
     for (int c = 0; c < hncl[b]; ++c) {
@@ -258,7 +267,6 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
       hcl[b * 16 + c].mask = k.mask;
       hcl[b * 16 + c].word = k.word;
       hcl[b * 16 + c].rev = k.reverse;
-      wmask |= 1u << k.word;
     }
   }
   e = cudaMemcpyAsync(W + w.cl, hcl, clb, cudaMemcpyHostToDevice, st);
@@ -287,9 +295,10 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   p.V = V;
   p.nvec = nvec;
   p.K = K;
-  p.wmask = wmask;
+  p.wmax = max_word(cl, off, B);
   p.cl = (const KClause*)(W + w.cl);
   p.ncl = (const int*)(W + w.ncl);
+  p.maxc = max_clauses(off, B);
   p.dbg = nullptr;
   // 1. sample pass (no threshold)
   p.thr = nullptr;
@@ -379,7 +388,7 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   if (rc != LINR_OK) return fail(rc, why);
   if (mode == 0 && (!out_ids || !out_scores)) return fail(LINR_EINVAL, "null outputs");
   if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
-  if (use_tc(ix, B, V) && !ix->force_gemv)
+  if (use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) && !ix->force_gemv)
     return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
   Plan pl;
   if (!make_plan(ix, B, V, K, &pl, &why)) return fail(LINR_EUNSUPPORTED, why);
@@ -673,7 +682,7 @@ size_t linr_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, i
   Plan pl;
   std::string why;
   size_t n = 0;
-  if (use_tc(ix, B, V)) {
+  if (use_tc(ix, B, V, 0, 1)) {   // clause-light bound: the batched path may be taken
     TcWs w;
     if (tc_layout(ix, B, V, K, &w, &why)) n = w.end;
   }

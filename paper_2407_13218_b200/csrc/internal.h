@@ -115,9 +115,10 @@ struct TcParams {
   const DevHeader* hdr;
   uint32_t row0;
   int nu, V, nvec, K;
-  uint32_t wmask;
+  int wmax;              // attribute words staged per tile (1 + highest word any clause reads; 0 = none)
   const KClause* cl;     // [nu][16]
   const int* ncl;        // [nu]
+  int maxc;              // clause slots per user in the shared-memory table (max clauses of any user)
   const uint64_t* thr;   // [nu] (main pass) ; null in the sample pass (T = 0)
   uint64_t* buf;         // [nu][grid][cap] per-(user, CTA) regions
   int cap;
@@ -128,7 +129,7 @@ struct TcParams {
 
 bool tc_supported(int dtype, int dim, int nvec, int V);
 int tc_np(int nvec);
-size_t tc_smem_bytes(int dtype, int dim, int np, int nu);
+size_t tc_smem_bytes(int dtype, int dim, int np, int nu, int maxc, int wmax);
 bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes, int box_rows);
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st);
 cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
@@ -139,8 +140,8 @@ cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int
 cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
                             const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
                             cudaStream_t st);
-constexpr int kTcSampleTiles = 2;
-constexpr int kTcSampleCap = kTcSampleTiles * 128;   // per (user, CTA) region: cannot overflow
+constexpr int kTcSampleTiles = 8;
+constexpr int kTcSampleCap = 256;   // per (user, CTA) region of the sample: first passers in row order
 constexpr int kTcMainCap = 256;                      // per (user, CTA) region of the main pass
 
 

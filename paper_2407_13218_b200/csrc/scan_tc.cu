@@ -29,10 +29,11 @@
 
 namespace linr {
 
-constexpr int kTcThreads = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
-constexpr int kTcXStagesMax = 4;  // item-tile ring (released by the MMA commit); 3 when the queries are large
-constexpr int tc_xstages(int np, int rowb) { return (size_t)np * rowb + (size_t)4 * 128 * rowb > 160 * 1024 ? 3 : 4; }
-constexpr int kTcAStages = 4;     // attribute ring (released by the epilogue)
+constexpr int kTcThreads = 640;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-19 epilogue (4 column groups)
+constexpr int kTcXStagesMax = 6;  // item-tile ring (released by the MMA commit): as many as shared memory holds
+constexpr int kTcAStages = 8;     // attribute ring (released by the epilogue): deeper than the item ring so
+                                  // the producer runs ahead of the epilogue by the item ring, not by this one
+constexpr size_t kTcSmemBudget = 232448;   // sm_100 opt-in dynamic shared memory per CTA
 constexpr int kTcRows = 128;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -100,6 +101,12 @@ LINR_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+LINR_DEV void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 LINR_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -161,48 +168,173 @@ struct TcSmemCtl {
   uint32_t tmem_base;
 };
 
-template <int DT, int D, int NP>
-struct TcLayout {
-  using G = TcGeom<DT, D>;
-  static constexpr size_t q_off = 0;                                        // NATOM x [NP][SW]
-  static constexpr size_t x_off = q_off + (size_t)NP * G::ROWB;             // XS x NATOM x [128][SW]
-  static constexpr int XS = tc_xstages(NP, G::ROWB);
-  static constexpr size_t a_off = x_off + (size_t)XS * G::XBYTES;   // AS x (4 words x 1 KB + 16 B)
-  static constexpr size_t a_stage = 4 * 1024 + 128;
-  static constexpr size_t thr_off = a_off + kTcAStages * a_stage;           // [nu] u64 keys, [nu] f32 scores
-  static constexpr size_t thrf_off(int nu) { return thr_off + ((size_t)nu * 8 + 15) / 16 * 16; }
-  static constexpr size_t scr_off(int nu) { return (thrf_off(nu) + (size_t)(nu + 31) / 32 * 32 * 4 + 127) / 128 * 128; }
-  static constexpr size_t scr_bytes = (size_t)(kTcThreads / 32 - 4) * 32 * 33 * 4;
-  static constexpr size_t cnt_off(int nu) { return scr_off(nu) + scr_bytes; }
-  static constexpr size_t ctl_off(int nu) { return cnt_off(nu) + ((size_t)nu * 4 + 15) / 16 * 16; }
-  static size_t bytes(int nu) { return ctl_off(nu) + sizeof(TcSmemCtl) + 1024; }   // + alignment slack
-};
+template <int CW>
+LINR_DEV void tmem_ld(uint32_t taddr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 32) tmem_ld32(taddr, v);
+  else if constexpr (CW == 16) tmem_ld16(taddr, v);
+  else tmem_ld8(taddr, v);
+}
+// max over n (compile-time) floats: tree of 3-input maxima
+template <int N>
+LINR_DEV float fmax_tree(const float* a);
+LINR_DEV float fmax3(float a, float b, float c);
+template <int N>
+LINR_DEV float fmax_tree(const float* a) {
+  if constexpr (N == 1) return a[0];
+  else if constexpr (N == 2) return fmaxf(a[0], a[1]);
+  else if constexpr (N == 3) return fmax3(a[0], a[1], a[2]);
+  else {
+    constexpr int M = (N + 2) / 3;
+    float b[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      if (3 * k + 2 < N) b[k] = fmax3(a[3 * k], a[3 * k + 1], a[3 * k + 2]);
+      else if (3 * k + 1 < N) b[k] = fmaxf(a[3 * k], a[3 * k + 1]);
+      else b[k] = a[3 * k];
+    }
+    return fmax_tree<M>(b);
+  }
+}
+LINR_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+template <bool kInt>
+LINR_DEV uint32_t vmax(uint32_t a, uint32_t b) {
+  if (kInt) return (uint32_t)max((int)a, (int)b);
+  return __float_as_uint(fmaxf(__uint_as_float(a), __uint_as_float(b)));
+}
 
+// Shared-memory layout (byte offsets from the 1 KB-aligned base). nu users, maxc clause slots per user,
+// npad = max(NP, 32) accumulator columns (a 32-column chunk never reads past the per-column tables).
+constexpr int kTcScrStride = 36;   // staged scores: [epilogue warp][kTcScrRows][36 words] (16B rows, no conflicts)
+constexpr int kTcScrRows = 4;      // hot rows staged per batch
+struct TcLay {
+  size_t q, qe, xe, x, a, astage, live, thr, ct, cq, cl, scr, cnt, ctl, bytes;
+  int xs;
+};
+// wmax = attribute words staged per tile (highest word any clause reads, + 1)
+__host__ __device__ inline TcLay tc_lay(int np, int rowb, int nu, int maxc, int wmax) {
+  TcLay l;
+  const int npad = np < 32 ? 32 : np;
+  l.q = 0;                                                       // NATOM x [NP][SW] queries (TMA)
+  l.qe = l.q + (size_t)np * rowb;                                // [npad][32 B] threshold K-step, B side
+  l.xe = (l.qe + (size_t)npad * 32 + 1023) / 1024 * 1024;        // [128][32 B] threshold K-step, A side
+  l.x = l.xe + 4096;                                             // xs x NATOM x [128][SW] item tiles
+  l.astage = (size_t)wmax * 1024 + 128;                          // wmax words x 1 KB + live bits (16 B)
+  l.live = (size_t)wmax * 1024;
+  size_t rest = (size_t)kTcAStages * l.astage;
+  rest += (size_t)nu * 8 + 16 + (size_t)npad * 8 + (size_t)nu * maxc * 16;
+  rest += (size_t)(kTcThreads / 32 - 4) * kTcScrRows * kTcScrStride * 4 + (size_t)nu * 4 + 16;
+  rest += sizeof(TcSmemCtl) + 1024;
+  const size_t tile = (size_t)kTcRows * rowb;
+  const size_t used = l.x + rest;
+  l.xs = used >= kTcSmemBudget ? 0 : (int)((kTcSmemBudget - used) / tile);
+  if (l.xs > kTcXStagesMax) l.xs = kTcXStagesMax;
+  l.a = l.x + (size_t)l.xs * tile;
+  l.thr = l.a + (size_t)kTcAStages * l.astage;                   // [nu] u64 threshold keys
+  l.ct = (l.thr + (size_t)nu * 8 + 15) / 16 * 16;                // [npad] per-column hot-test threshold
+  l.cq = l.ct + (size_t)npad * 4;                                // [npad] per-column score offset
+  l.cl = l.cq + (size_t)npad * 4;                                // [nu][maxc] clauses (16 B)
+  l.scr = l.cl + (size_t)nu * maxc * 16;                         // staged scores of hot rows
+  l.cnt = l.scr + (size_t)(kTcThreads / 32 - 4) * kTcScrRows * kTcScrStride * 4;   // [nu] region fill counters
+  l.ctl = (l.cnt + (size_t)nu * 4 + 15) / 16 * 16;
+  l.bytes = l.ctl + sizeof(TcSmemCtl) + 1024;                    // + alignment slack
+  return l;
+}
+
+// 16-bit encodings of the threshold K-step (kind::f16 operands)
+template <int DT>
+LINR_DEV uint16_t tc_h_one() { return DT == LINR_BF16 ? (uint16_t)0x3F80u : (uint16_t)0x3C00u; }
+template <int DT>
+LINR_DEV uint16_t tc_h_bits(float x) {   // exact for dtype values (the split halves and their negations)
+  if (DT == LINR_BF16) return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+  return __half_as_ushort(__float2half_rn(x));
+}
+template <int DT>
+LINR_DEV float tc_h_rd(float x) {
+  if (DT == LINR_BF16) return __bfloat162float(__float2bfloat16_rd(x));
+  return __half2float(__float2half_rd(x));
+}
+// Conservative folded threshold t_eff = hi + lo < T: two dtype values rounded down from the f32 value
+// just below T (about 16 (bf16) / 22 (f16) significant bits, so the hot band [t_eff, T) is thin).
+template <int DT>
+LINR_DEV void tc_h_split(float T, float* hi, float* lo) {
+  const float x = nextafterf(T, -INFINITY);
+  *hi = tc_h_rd<DT>(x);
+  *lo = tc_h_rd<DT>(x - *hi);   // x - hi is exact (Sterbenz-range) and >= 0
+}
+
+// Does row `arow` of the attribute stage satisfy all clauses of a user? (sCl row of maxc slots;
+// empty slots are always-true)
+LINR_DEV bool tc_clauses(const uint4* k, int maxc, const unsigned char* ad, int arow) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c < maxc) {
+      const uint4 kr = k[c];
+      const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
+      const uint64_t aw = reinterpret_cast<const uint64_t*>(ad + kr.z * 1024)[arow];
+      ok = ok && (((aw & mask) != 0ull) != (kr.w != 0u));
+    }
+  }
+  for (int c = 4; c < maxc; ++c) {
+    const uint4 kr = k[c];
+    const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
+    const uint64_t aw = reinterpret_cast<const uint64_t*>(ad + kr.z * 1024)[arow];
+    ok = ok && (((aw & mask) != 0ull) != (kr.w != 0u));
+  }
+  return ok;
+}
+
+// One CTA per SM, persistent over its tiles. Warp 0: TMA producer (item tile + attribute/live
+// stage per tile, queries once). Warp 1: MMA issuer (NKS K-steps over the tile, plus, for the
+// float kinds in the main pass, one extra K-step that adds -t_u to every column of user u so the
+// accumulator holds s - t). Warp 2: TMEM allocator. Warps 4..: epilogue.
+//
+// Sample pass (p.sample_tiles > 0, no thresholds): every passing (row, user) pair of the sampled
+// tiles is appended to the per-(user, CTA) regions (thread per row, clauses evaluated per pair).
+// Main pass: a row is hot when some column of the chunk reaches its threshold (float: max of the
+// folded s - t >= 0; int8: not every s - t negative). Hot rows are staged; the warp then walks
+// them, lane j taking column j: exact key >= T_u, clauses, append.
 template <int DT, int D, int NP>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_constant__ TcParams p) {
   using G = TcGeom<DT, D>;
-  using Lay = TcLayout<DT, D, NP>;
   constexpr bool kInt = DT == LINR_I8;
   constexpr int NEPI = kTcThreads - 128;   // epilogue threads (warps 4..)
+  constexpr int NPAD = NP < 32 ? 32 : NP;
+  // epilogue chunk width: 32 columns, narrower for small NP so all four column groups get work
+  constexpr int CW = NP >= 128 ? 32 : (NP == 64 ? 16 : 8);
   extern __shared__ __align__(1024) unsigned char smem_raw_tc[];
   // 1024-byte alignment for the 128B-swizzled TMA/UMMA tiles; indexing the extern array keeps the
   // pointers in the shared window (LDS/STS rather than generic loads)
   unsigned char* smem = smem_raw_tc + ((1024u - (smem_u32(smem_raw_tc) & 1023u)) & 1023u);
-  unsigned char* sQ = smem + Lay::q_off;
-  unsigned char* sX = smem + Lay::x_off;
-  unsigned char* sA = smem + Lay::a_off;
-  uint64_t* sThr = reinterpret_cast<uint64_t*>(smem + Lay::thr_off);
-  float* sThrF = reinterpret_cast<float*>(smem + Lay::thrf_off(p.nu));   // padded to 32 users, 16B aligned
-  TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + Lay::ctl_off(p.nu));
-  float* scratch = reinterpret_cast<float*>(smem + Lay::scr_off(p.nu));
-  int* sCnt = reinterpret_cast<int*>(smem + Lay::cnt_off(p.nu));
+  const TcLay L = tc_lay(NP, G::ROWB, p.nu, p.maxc, p.wmax);
+  const int XS = L.xs;
+  unsigned char* sQ = smem + L.q;
+  unsigned char* sQe = smem + L.qe;
+  unsigned char* sXe = smem + L.xe;
+  unsigned char* sX = smem + L.x;
+  unsigned char* sA = smem + L.a;
+  uint64_t* sThr = reinterpret_cast<uint64_t*>(smem + L.thr);
+  uint32_t* sCT = reinterpret_cast<uint32_t*>(smem + L.ct);   // hot-test threshold per column (f32 or i32 bits)
+  float* sCQ = reinterpret_cast<float*>(smem + L.cq);         // rare path: score = acc + sCQ (folded) / T (int)
+  uint32_t* sScr = reinterpret_cast<uint32_t*>(smem + L.scr);
+  uint4* sCl = reinterpret_cast<uint4*>(smem + L.cl);
+  int* sCnt = reinterpret_cast<int*>(smem + L.cnt);
+  TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + L.ctl);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t sFreeChunks;   // main pass: chunks holding a user without a threshold
 
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
   const int64_t ntiles = (hwm + kTcRows - 1) / kTcRows;
   // tile sequence of this CTA: the sample pass takes sample_tiles distinct tiles per CTA spread
   // evenly over the index (every tile once if the index is smaller); the main pass strides.
   const bool sample = p.sample_tiles > 0;
+  const bool fold = !kInt && !sample;
+  const int V = p.V;   // 1, 2, 4 or 8
+  const int lv = V == 1 ? 0 : (V == 2 ? 1 : (V == 4 ? 2 : 3));
   const int64_t stotal = (int64_t)gridDim.x * p.sample_tiles;
   int64_t nmine;
   if (sample) {
@@ -220,7 +352,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   };
 
   if (tid == 0) {
-    for (int s = 0; s < Lay::XS; ++s) {
+    for (int s = 0; s < XS; ++s) {
       mbar_init(&ctl->xfull[s], 1);
       mbar_init(&ctl->xempty[s], 1);   // released by the MMA commit
     }
@@ -234,18 +366,70 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
     }
     mbar_init(&ctl->qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sFreeChunks = 0u;
   }
-  for (int u = tid; u < p.nu; u += kTcThreads) sCnt[u] = 0;
-  for (int u = tid; u < (p.nu + 31) / 32 * 32; u += kTcThreads) {
-    if (u < p.nu) {
-      const uint64_t T = p.thr ? p.thr[u] : 0ull;
-      sThr[u] = T;
-      sThrF[u] = T ? key_score(T) : -INFINITY;   // score part of the threshold (ties: full key check)
+  for (int u = tid; u < p.nu; u += kTcThreads) {
+    sCnt[u] = 0;
+    sThr[u] = p.thr ? p.thr[u] : 0ull;
+  }
+  // clause table [nu][maxc]; missing slots hold an always-true clause (empty mask, reverse)
+  for (int idx = tid; idx < p.nu * p.maxc; idx += kTcThreads) {
+    const int u = idx / p.maxc, c = idx - u * p.maxc;
+    uint4 k = make_uint4(0u, 0u, 0u, 1u);
+    if (c < p.ncl[u]) k = *reinterpret_cast<const uint4*>(p.cl + u * 16 + c);
+    sCl[idx] = k;
+  }
+  __syncthreads();
+  // per-column thresholds. Folded (float main pass): t_eff = hi + lo < T_u (tc_h_split), the MMA adds
+  // -t_eff, the hot test is acc >= 0 and the rare path rebuilds s = acc + t_eff. A user without a
+  // threshold (T = 0) gets t_eff = 0 and marks its chunk always-hot. Columns past the users get a
+  // huge t_eff (never hot). Int8: i32 threshold ceil(T) clamped to +-2^30 (s - t never overflows).
+  for (int c = tid; c < NPAD; c += kTcThreads) {
+    const int u = c >> lv;
+    const bool real = c < p.nvec;
+    const uint64_t T = real ? sThr[u] : 0ull;
+    uint32_t ct;
+    float cq;
+    if (kInt) {
+      const float tf = T ? key_score(T) : -INFINITY;
+      ct = (uint32_t)(!real ? (1 << 30) : (T ? (int)fmaxf(fminf(ceilf(tf), 1073741824.0f), -1073741824.0f) : -(1 << 30)));
+      cq = real ? tf : INFINITY;
+    } else if (fold) {
+      float hi = 0.0f, lo = 0.0f;
+      if (!real) {
+        hi = DT == LINR_BF16 ? 3.0e38f : 65504.0f;
+      } else if (T && fabsf(key_score(T)) < 16384.0f) {
+        tc_h_split<DT>(key_score(T), &hi, &lo);
+      } else {   // no threshold (or out of the 16-bit range): t_eff = 0, the chunk is always hot
+        atomicOr(&sFreeChunks, 1u << (c / CW));
+      }
+      ct = __float_as_uint(0.0f);
+      cq = hi + lo;   // <= the f32 value below T: a non-hot pair rebuilds to a score < T
+      uint16_t* qe = reinterpret_cast<uint16_t*>(sQe) + c * 16 + (((c >> 2) & 1) << 3);
+      qe[0] = tc_h_bits<DT>(-hi);
+      qe[1] = tc_h_bits<DT>(-lo);
     } else {
-      sThrF[u] = INFINITY;                        // padding users never qualify
+      ct = __float_as_uint(!real ? INFINITY : (T ? key_score(T) : -INFINITY));
+      cq = 0.0f;
     }
+    sCT[c] = ct;
+    sCQ[c] = cq;
   }
-  constexpr uint32_t kCols = (2 * NP) <= 32 ? 32 : ((2 * NP) <= 64 ? 64 : ((2 * NP) <= 128 ? 128 : ((2 * NP) <= 256 ? 256 : 512)));
+  if (fold) {
+    // threshold K-step operands in the 32-byte swizzle (16-byte chunk h of row r at h ^ ((r >> 2) & 1)):
+    // A = [1, 1, 0, ...] for every item row, B = [-hi, -lo, 0, ...] per column (written above)
+    for (int i = tid; i < NPAD * 16; i += kTcThreads) {
+      const int c = i >> 4, e = (i & 15) - (((c >> 2) & 1) << 3);   // logical element of the slot
+      if (e != 0 && e != 1) reinterpret_cast<uint16_t*>(sQe)[i] = 0;
+    }
+    for (int i = tid; i < kTcRows * 16; i += kTcThreads) {
+      const int r = i >> 4, e = (i & 15) - (((r >> 2) & 1) << 3);
+      reinterpret_cast<uint16_t*>(sXe)[i] = (e == 0 || e == 1) ? tc_h_one<DT>() : (uint16_t)0;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+  }
+  // two accumulators of NP columns; a 32-column chunk load of the second stays inside (NP = 16: 64)
+  constexpr uint32_t kCols = (2 * NP) <= 64 ? 64 : ((2 * NP) <= 128 ? 128 : ((2 * NP) <= 256 ? 256 : 512));
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&ctl->tmem_base)),
                  "n"(kCols)
@@ -262,13 +446,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       // queries once: NATOM boxes of [NP rows x SW bytes]
       mbar_expect_tx(&ctl->qbar, (uint32_t)(NP * G::ROWB));
       for (int a = 0; a < G::NATOM; ++a) tma_load_2d(sQ + (size_t)a * NP * G::SW, &p.tmq, a * G::SW, 0, &ctl->qbar);
-      uint32_t abytes = 16u;
-      for (int w = 0; w < 4; ++w)
-        if ((p.wmask >> w) & 1u) abytes += 1024u;
+      const uint32_t abytes = (uint32_t)p.wmax * 1024u + 16u;
+      int xs = 0;
+      uint32_t xph = 0;
       for (int64_t i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
-        const int xs = (int)(i % Lay::XS), as = (int)(i % kTcAStages);
-        const uint32_t xph = (uint32_t)((i / Lay::XS) & 1), aph = (uint32_t)((i / kTcAStages) & 1);
+        const int as = (int)(i % kTcAStages);
+        const uint32_t aph = (uint32_t)((i / kTcAStages) & 1);
         mbar_wait(&ctl->xempty[xs], xph ^ 1u);
         if (p.dbg && blockIdx.x == 0 && i < 64) p.dbg[i * 4 + 0] = gtimer();
         unsigned char* xd = sX + (size_t)xs * G::XBYTES;
@@ -276,12 +460,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         for (int a = 0; a < G::NATOM; ++a)
           tma_load_2d(xd + (size_t)a * kTcRows * G::SW, &p.tmx, a * G::SW, (int)(t * kTcRows), &ctl->xfull[xs]);
         mbar_wait(&ctl->aempty[as], aph ^ 1u);
-        unsigned char* ad = sA + (size_t)as * Lay::a_stage;
+        unsigned char* ad = sA + (size_t)as * L.astage;
         mbar_expect_tx(&ctl->afull[as], abytes);
-        for (int w = 0; w < 4; ++w)
-          if ((p.wmask >> w) & 1u)
-            bulk_load(ad + w * 1024, p.attr + (size_t)w * p.cap_pad + t * kTcRows, 1024u, &ctl->afull[as]);
-        bulk_load(ad + 4 * 1024, p.live + t * (kTcRows / 32), 16u, &ctl->afull[as]);
+        for (int w = 0; w < p.wmax; ++w)
+          bulk_load(ad + w * 1024, p.attr + (size_t)w * p.cap_pad + t * kTcRows, 1024u, &ctl->afull[as]);
+        bulk_load(ad + L.live, p.live + t * (kTcRows / 32), 16u, &ctl->afull[as]);
+        if (++xs == XS) { xs = 0; xph ^= 1u; }
       }
     }
   } else if (warp == 1) {
@@ -290,9 +474,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       mbar_wait(&ctl->qbar, 0);
       tc_fence_after();
       const uint32_t q_s = smem_u32(sQ);
+      const uint64_t dxe = umma_desc<32>(smem_u32(sXe)), dqe = umma_desc<32>(smem_u32(sQe));
+      int xs = 0;
+      uint32_t xph = 0;
       for (int64_t i = 0; i < nmine; ++i) {
-        const int xs = (int)(i % Lay::XS);
-        const uint32_t xph = (uint32_t)((i / Lay::XS) & 1);
         const int acc = (int)(i & 1);
         const uint32_t tph = (uint32_t)((i >> 1) & 1);
         mbar_wait(&ctl->tempty[acc], tph ^ 1u);
@@ -307,20 +492,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           const uint64_t db = umma_desc<G::SW>(q_s + (uint32_t)(atom * NP * G::SW + kk * G::KSTEP_B));
           tc_mma<DT>(tmem + (uint32_t)(acc * NP), da, db, idesc, k > 0 ? 1u : 0u);
         }
+        if (fold) tc_mma<DT>(tmem + (uint32_t)(acc * NP), dxe, dqe, idesc, 1u);
         tc_commit(&ctl->xempty[xs]);  // item tile reusable once the MMAs have read it
         tc_commit(&ctl->tfull[acc]);  // accumulator ready
+        if (++xs == XS) { xs = 0; xph ^= 1u; }
       }
     }
   } else if (warp >= 4) {
-    // ---- epilogue: thread <-> TMEM lane (item row) (warp % 4) * 32 + lane; the two epilogue
+    // ---- epilogue: thread <-> TMEM lane (item row) (warp % 4) * 32 + lane; the epilogue
     // warpgroups split the accumulator columns in 32-column chunks (each chunk = 32/V users).
     const int row = (warp & 3) * 32 + lane;
     const int grp = (warp - 4) >> 2;
     constexpr int NGRP = NEPI / 128;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int V = p.V;                       // 1, 2, 4 or 8
-    const int lv = V == 1 ? 0 : (V == 2 ? 1 : (V == 4 ? 2 : 3));
-    const int nchunks = (p.nvec + 31) / 32;
+    const int nchunks = (p.nvec + CW - 1) / CW;
+    const uint32_t free_chunks = sFreeChunks;
+    uint32_t* scr = sScr + (size_t)(warp - 4) * kTcScrRows * kTcScrStride;
     for (int64_t i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int as = (int)(i % kTcAStages);
@@ -331,97 +518,125 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       mbar_wait(&ctl->afull[as], aph);
       tc_fence_after();
       if (p.dbg && blockIdx.x == 0 && i < 64 && tid == 128) p.dbg[i * 4 + 2] = gtimer();
-      const unsigned char* ad = sA + (size_t)as * Lay::a_stage;
-      const uint32_t lw = reinterpret_cast<const uint32_t*>(ad + 4 * 1024)[row >> 5];
+      const unsigned char* ad = sA + (size_t)as * L.astage;
+      const uint32_t lw = reinterpret_cast<const uint32_t*>(ad + L.live)[row >> 5];
       const bool live = ((lw >> (row & 31)) & 1u) && (t * kTcRows + row < hwm);
-      const uint32_t gid = p.row0 + (uint32_t)(t * kTcRows + row);
+      const uint32_t rbase = p.row0 + (uint32_t)(t * kTcRows) + (uint32_t)((warp & 3) * 32);
       for (int ch = grp; ch < nchunks; ch += NGRP) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(acc * NP + ch * 32), v);
-        const int u0 = (ch * 32) >> lv;
-        float sc[32];
+        uint32_t v[CW];
+        tmem_ld<CW>(tmem + lane_base + (uint32_t)(acc * NP + ch * CW), v);
+        const int c0 = ch * CW;
+        if (p.dbg && blockIdx.x == 0 && i == 0 && c0 < 32) {   // diagnostics: raw accumulator of tile 0
+          uint32_t* d32 = reinterpret_cast<uint32_t*>(p.dbg + 1024);
+          for (int j = 0; j < CW; ++j) d32[row * 32 + c0 + j] = v[j];
+          if (row == 0)
+            for (int j = 0; j < CW; ++j) d32[128 * 32 + c0 + j] = __float_as_uint(sCQ[c0 + j]);
+        }
+        if (V > 1) {   // per-user max over its V aligned columns into the user's first column
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sc[j] = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
-        // candidate mask: bit j = first column of a user whose max reaches the user's threshold score
-        uint32_t cm = 0;
-        if (V == 1) {
-          const float4* tf = reinterpret_cast<const float4*>(sThrF + u0);   // u0 % 32 == 0: aligned
-#pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 t4 = tf[j4];
-            cm |= (sc[4 * j4] >= t4.x ? 1u : 0u) << (4 * j4);
-            cm |= (sc[4 * j4 + 1] >= t4.y ? 1u : 0u) << (4 * j4 + 1);
-            cm |= (sc[4 * j4 + 2] >= t4.z ? 1u : 0u) << (4 * j4 + 2);
-            cm |= (sc[4 * j4 + 3] >= t4.w ? 1u : 0u) << (4 * j4 + 3);
-          }
-        } else {
-          // max over each user's V in {2,4,8} aligned columns: butterfly inside groups of V
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) { const float m = fmaxf(sc[j], sc[j + 1]); sc[j] = m; sc[j + 1] = m; }
+          for (int j = 0; j < CW; j += 2) v[j] = vmax<kInt>(v[j], v[j + 1]);
           if (V >= 4) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float m0 = fmaxf(sc[j], sc[j + 2]);
-              sc[j] = m0; sc[j + 1] = m0; sc[j + 2] = m0; sc[j + 3] = m0;
-            }
+            for (int j = 0; j < CW; j += 4) v[j] = vmax<kInt>(v[j], v[j + 2]);
           }
           if (V >= 8) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              const float m0 = fmaxf(sc[j], sc[j + 4]);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) sc[j + k] = m0;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            if ((j & (V - 1)) != 0) continue;
-            cm |= (sc[j] >= sThrF[u0 + (j >> lv)] ? 1u : 0u) << j;
+            for (int j = 0; j < CW; j += 8) v[j] = vmax<kInt>(v[j], v[j + 4]);
           }
         }
-        if (!live) cm = 0u;
-        uint32_t wor = __reduce_or_sync(0xffffffffu, cm);
-        if (wor == 0u) continue;
-        // rare: stage this lane's scores, then visit only the users some lane flagged
-        float* scr = scratch + (size_t)(warp - 4) * 32 * 33 + lane * 33;
+        if (sample) {
+          // ---- sample pass: thread per row, every passing user of the chunk
+          if (live) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) scr[j] = sc[j];
-        __syncwarp();
-        while (wor) {
-          const int j = __ffs(wor) - 1;
-          wor &= wor - 1u;
-          const int u = u0 + (j >> lv);
-          const bool flagged = (cm >> j) & 1u;
-          bool cand = false;
-          uint64_t key = 0ull;
-          if (flagged) {
-            const float m = scr[j];
-            key = make_key(m, gid);
-            if (key >= sThr[u]) {
-              cand = true;
-              const int nc = __ldg(p.ncl + u);
-              for (int c = 0; c < nc && cand; ++c) {
-                const uint4 kr = __ldg(reinterpret_cast<const uint4*>(p.cl) + u * 16 + c);
-                const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
-                const uint64_t aw = reinterpret_cast<const uint64_t*>(ad + kr.z * 1024)[row];
-                const bool hit = (aw & mask) != 0ull;
-                if (hit == (kr.w != 0u)) cand = false;
+            for (int j = 0; j < CW; ++j) {
+              if ((j & (V - 1)) != 0 || c0 + j >= p.nvec) continue;
+              const int u = (c0 + j) >> lv;
+              if (!tc_clauses(sCl + u * p.maxc, p.maxc, ad, row)) continue;
+              const float sj = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
+              const int pos = atomicAdd(&sCnt[u], 1);
+              if (pos < p.cap) p.buf[((size_t)u * gridDim.x + blockIdx.x) * p.cap + pos] = make_key(sj, rbase + lane);
+            }
+          }
+          continue;
+        }
+        // ---- main pass: hot-row test (a user's first column holds its max; the others are <= it,
+        // so testing every column is equivalent)
+        bool hot;
+        const uint4* ct4 = reinterpret_cast<const uint4*>(sCT + c0);
+        if (kInt) {
+          uint32_t n4[CW / 4];
+#pragma unroll
+          for (int j4 = 0; j4 < CW / 4; ++j4) {
+            const uint4 t4 = ct4[j4];
+            n4[j4] = (uint32_t)((int)v[4 * j4] - (int)t4.x) & (uint32_t)((int)v[4 * j4 + 1] - (int)t4.y) &
+                     (uint32_t)((int)v[4 * j4 + 2] - (int)t4.z) & (uint32_t)((int)v[4 * j4 + 3] - (int)t4.w);
+          }
+          uint32_t neg = n4[0];
+#pragma unroll
+          for (int j4 = 1; j4 < CW / 4; ++j4) neg &= n4[j4];
+          hot = (neg >> 31) == 0u;
+        } else if (fold) {
+          float f[CW];
+#pragma unroll
+          for (int j = 0; j < CW; ++j) f[j] = __uint_as_float(v[j]);
+          hot = fmax_tree<CW>(f) >= 0.0f || ((free_chunks >> ch) & 1u);
+        } else {
+          float f[CW];
+#pragma unroll
+          for (int j = 0; j < CW; ++j) f[j] = __uint_as_float(v[j]) - __uint_as_float(sCT[c0 + j]);
+          hot = fmax_tree<CW>(f) >= 0.0f;
+        }
+        hot = hot && live;
+        uint32_t fl = __ballot_sync(0xffffffffu, hot);
+        if (fl == 0u) continue;
+        // rare: hot rows are staged in batches of kTcScrRows; one staged row at a time, lane j < CW
+        // takes column c0 + j (the first column of its user), rebuilds the exact score, checks the
+        // full key and the clauses, appends.
+        const int cj = c0 + lane;
+        const int uj = cj >> lv;
+        const bool lead = lane < CW && (lane & (V - 1)) == 0 && cj < p.nvec;
+        const float cq = lead ? sCQ[cj] : 0.0f;
+        const bool freej = fold && lead && sThr[uj] == 0ull;   // user without a threshold
+        while (fl) {
+          const uint32_t nth = __fns(fl, 0, kTcScrRows + 1);   // position of the (kTcScrRows+1)-th hot row
+          const uint32_t batch = nth == 0xffffffffu ? fl : (fl & ((1u << nth) - 1u));
+          fl &= ~batch;
+          if ((batch >> lane) & 1u) {
+            uint32_t* dst = scr + __popc(batch & lanemask_lt()) * kTcScrStride;
+#pragma unroll
+            for (int q4 = 0; q4 < CW / 4; ++q4)
+              *reinterpret_cast<uint4*>(dst + 4 * q4) = make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+          }
+          __syncwarp();
+          uint32_t bb = batch;
+          for (int k = 0; bb; ++k) {
+            const int r = __ffs(bb) - 1;
+            bb &= bb - 1u;
+            if (!lead) continue;
+            const uint32_t raw = scr[k * kTcScrStride + lane];
+            float sj;
+            bool q;
+            if (kInt) {
+              sj = (float)(int)raw;
+              q = sj >= cq;
+            } else if (fold) {
+              const float a = __uint_as_float(raw);
+              sj = a + cq;
+              q = a >= 0.0f || freej;
+            } else {
+              sj = __uint_as_float(raw);
+              q = sj >= __uint_as_float(sCT[cj]);
+            }
+            if (q) {
+              const uint64_t key = make_key(sj, rbase + (uint32_t)r);
+              if (key >= sThr[uj] && tc_clauses(sCl + uj * p.maxc, p.maxc, ad, (warp & 3) * 32 + r)) {
+                const int pos = atomicAdd(&sCnt[uj], 1);
+                if (pos < p.cap) p.buf[((size_t)uj * gridDim.x + blockIdx.x) * p.cap + pos] = key;
               }
             }
           }
-          const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-          if (bal) {   // this CTA's region of user u: shared-memory counter, fire-and-forget stores
-            const int leader = __ffs(bal) - 1;
-            int pos0 = 0;
-            if (lane == leader) pos0 = atomicAdd(&sCnt[u], __popc(bal));
-            pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-            if (cand) {
-              const int pos = pos0 + __popc(bal & lanemask_lt());
-              if (pos < p.cap) p.buf[((size_t)u * gridDim.x + blockIdx.x) * p.cap + pos] = key;
-            }
-          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&ctl->tempty[acc]);
@@ -467,6 +682,7 @@ __device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int
 
 // ------------------------------------------------------------------ thresholds from the sample
 constexpr int kTcGatherCap = 16384;
+constexpr double kTcSigma = 4.0;
 __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sbuf, const int* scnt, int scap,
                                                               int grid, int nu, int K, int sample_items,
                                                               const DevHeader* hdr, uint64_t* thr) {
@@ -477,12 +693,18 @@ __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sb
   uint64_t* keys = reinterpret_cast<uint64_t*>(tsm + ((sizeof(SelScratch) + 32 + 15) & ~size_t(15)));
   const int u = blockIdx.x;
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&hdr->hwm);
-  const double frac = hwm > 0 ? (double)sample_items / (double)hwm : 1.0;
-  const double lam = (double)K * (frac < 1.0 ? frac : 1.0);
-  const int r = (int)ceil(lam + 6.0 * sqrt(lam) + 3.0);
   long long total = 0;
-  // any subset of the sample gives a valid (smaller or equal) r-th key
+  // regions (and the gather) keep the first passers in row order: a subset of the sample whose
+  // size fraction n/total scales the expected count of global top-K keys it holds
   const int n = gather_regions<512>(sbuf, scnt, grid, scap, u, keys, kTcGatherCap, s_n, s_total, &total);
+  double frac = hwm > 0 ? (double)sample_items / (double)hwm : 1.0;
+  frac = frac < 1.0 ? frac : 1.0;
+  if (total > n && total > 0) frac *= (double)n / (double)total;
+  // lam = expected sample keys among the global top K; r sits kTcSigma deviations above it, so the
+  // r-th sample key is below the global K-th key except with a small probability (caught exactly by
+  // the finalisation's certification, which sends the user to the exact GEMV path)
+  const double lam = (double)K * frac;
+  const int r = (int)ceil(lam + kTcSigma * sqrt(lam) + 3.0);
   uint64_t T = 0ull;
   if (n >= r) T = block_select_ge<512>([keys](int i) { return keys[i]; }, n, r, sc);
   if (threadIdx.x == 0) thr[u] = T;
@@ -601,8 +823,7 @@ bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes,
 
 template <int DT, int D, int NP>
 static cudaError_t launch_tc_np(const TcParams& p, int grid, cudaStream_t st) {
-  using Lay = TcLayout<DT, D, NP>;
-  const size_t smem = Lay::bytes(p.nu);
+  const size_t smem = tc_lay(NP, TcGeom<DT, D>::ROWB, p.nu, p.maxc, p.wmax).bytes;
   auto k = tc_scan_kernel<DT, D, NP>;
   static size_t set = 0;
   if (smem > set) {
@@ -638,12 +859,10 @@ int tc_np(int nvec) {
   while (np < nvec) np <<= 1;
   return np;
 }
-size_t tc_smem_bytes(int dtype, int dim, int np, int nu) {
+size_t tc_smem_bytes(int dtype, int dim, int np, int nu, int maxc, int wmax) {
   const int esz = dtype == LINR_I8 ? 1 : 2;
-  const int rowb = dim * esz;
-  return (size_t)np * rowb + (size_t)tc_xstages(np, rowb) * kTcRows * rowb + kTcAStages * (4 * 1024 + 128) +
-         (size_t)nu * 8 + 16 + (size_t)(nu + 31) / 32 * 32 * 4 + 128 + (size_t)(kTcThreads / 32 - 4) * 32 * 33 * 4 +
-         (size_t)nu * 4 + 16 + sizeof(TcSmemCtl) + 1024;
+  const TcLay l = tc_lay(np, dim * esz, nu, maxc, wmax);
+  return l.xs >= 2 ? l.bytes : (size_t)-1;   // at least double-buffered item tiles
 }
 
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st) {

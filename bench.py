@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--items", type=int, default=N_ITEMS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pass-counts", action="store_true", help="batched path: also compute per-query pass counts")
+    ap.add_argument("--pipeline", type=int, default=2,
+                    help="searches in flight on separate streams in the throughput region (1 = serial)")
     return ap.parse_args()
 
 
@@ -106,12 +108,14 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per scan launch from the committed ncu --set full summary, if present."""
+def ncu_traffic(workload):
+    """dram bytes per scan launch from the committed ncu --set full summary of the same workload
+    (profiles/scan_traffic.json: {workload name: {...}}), else None."""
     p = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            e = json.load(open(p)).get(workload)
+            return e.get("dram_bytes_per_launch") if e else None
         except Exception:
             return None
     return None
@@ -219,10 +223,12 @@ def run_gpu(args):
     sc = torch.empty((args.batch, K), dtype=torch.float32, device=dev)
     ps = torch.empty(args.batch, dtype=torch.int64, device=dev)
 
+    want_pass = args.batch <= 8 or args.pass_counts
+
     def step():
         if sidx is not None:
             return sidx.search(qd, cls, K)
-        return ix.search(qd, cls, K, out=(ids, sc, ps), want_pass=args.batch <= 8 or args.pass_counts)
+        return ix.search(qd, cls, K, out=(ids, sc, ps), want_pass=want_pass)
 
     for _ in range(args.warmup):
         step()
@@ -231,30 +237,57 @@ def run_gpu(args):
     torch.cuda.synchronize()
     pass_count = int(r0[2][0].item())
 
-    # ---------------- device-timed region
     stream = torch.cuda.current_stream(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = Clocks(local)
-    time.sleep(0.3)
+
+    def timed(steps, pipe):
+        """Device time of `steps` searches: pipe = 1 serial on one stream; pipe > 1 round-robin over
+        pipe streams, each with its own workspace and outputs (pipelined serving: a search's merge
+        tail overlaps the next search's scan). Returns ms."""
+        streams = [stream] + [torch.cuda.Stream(dev) for _ in range(pipe - 1)]
+        wss = [ix.workspace(args.batch, 1, K)] + [ix.new_workspace(args.batch, 1, K) for _ in range(pipe - 1)]
+        outs = [(ids, sc, ps)] + [(torch.empty_like(ids), torch.empty_like(sc), torch.empty_like(ps))
+                                  for _ in range(pipe - 1)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for s_ in streams[1:]:
+            s_.wait_event(e0)
+        for k in range(steps):
+            if sidx is not None:
+                step()
+                continue
+            j = k % pipe
+            with torch.cuda.stream(streams[j]):
+                ix.search(qd, cls, K, out=outs[j], want_pass=want_pass, ws=wss[j])
+        for s_ in streams[1:]:
+            ej = torch.cuda.Event()
+            ej.record(s_)
+            stream.wait_event(ej)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return e0.elapsed_time(e1)
+
+    # ---------------- serial latency (kernel timed alone: the roofline's launch durations)
     ix.profile(True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    lat_ms = timed(args.steps, 1) / args.steps
     prof = ix.profile_read()
     ix.profile(False)
+    # ---------------- device-timed throughput region
+    pipe = args.pipeline if sidx is None else 1
+    for _ in range(3):
+        timed(2 * pipe, pipe)   # warm the extra streams / workspaces
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    ms = timed(args.steps, pipe)
     clk = clocks.stop()
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms, lat_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, lat_ms = float(t[0].item()), float(t[1].item())
     ms_step = ms / args.steps
 
     # ---------------- e2e through the host-buffer public API
@@ -298,7 +331,7 @@ def run_gpu(args):
     if alg_bytes is not None and scan_ms > 0:
         ach = alg_bytes / (scan_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(), "kernel": "scan_gemv_kernel<bf16,128,1>",
+                "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": "scan_gemv_kernel<bf16,128,1>",
                 "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                 "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
@@ -342,6 +375,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (datagen recipe, generated on device)",
             "qps": args.batch / (ms_step / 1e3),
+            "latency_ms": lat_ms, "pipeline": pipe,
             "config": {"workload": workload_name(args, n_local), "n_items_per_gpu": n_local, "n_items_total": n_total,
                        "batch": args.batch, "K": K, "dim": DIM, "preset": args.preset, "pass_count": pass_count,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",

@@ -21,8 +21,10 @@
  *  - `stream` is a cudaStream_t passed as void*. All device work is enqueued on it; calls
  *    return before the work finishes, except linr_search_host and linr_index_stats, which
  *    synchronise `stream`. A search observes exactly the updates enqueued before it on the same
- *    stream (snapshot consistency by stream order; reading R16). Unordered concurrent use of one
- *    index from two streams is undefined.
+ *    stream (snapshot consistency by stream order; reading R16). Searches (only searches) of one
+ *    index may run concurrently on different streams, up to 16 in flight, each with its own
+ *    workspace (pipelined serving); any other unordered concurrent use of one index from two
+ *    streams (an update racing a search) is undefined.
  *  - Item ids are global row ids: local row r of a shard has id global_row0 + r (int64 in the
  *    ABI, < 2^32-1 internally). Results are ordered by score descending, then id ascending
  *    (reading R5); slots past min(K, pass_count) hold id -1 and score -inf (reading R6).

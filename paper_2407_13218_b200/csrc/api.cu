@@ -84,6 +84,7 @@ struct linr_index {
   std::vector<ProfEvents> prof_used, prof_free;
   int64_t prof_launches = 0;
   int64_t tc_fallbacks = 0;     // batched-path users recomputed on the GEMV path
+  uint64_t fuse_seq = 0;        // fused-merge ticket slot rotation
   bool force_gemv = false;
   int64_t cap_pad;
   int rowbytes;
@@ -156,7 +157,9 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
     pl->C = (int)C;
     pl->bufcap = (int)C + head;
     pl->smem = std::max(fixed + (size_t)nu * pl->bufcap * 8, merge_smem());
-    pl->grid = ix->num_sms;
+    // one launch with a fused merge: leave one SM free so the merging CTA of this search and the
+    // scan of a search issued on another stream overlap without a straggler CTA
+    pl->grid = (pl->groups == 1 && ix->num_sms > 1) ? ix->num_sms - 1 : ix->num_sms;
     pl->list_cap = (B <= 8) ? pl->bufcap : std::min(pl->bufcap, std::max(2 * K, 2048));
     return true;
   }
@@ -478,6 +481,7 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
     }
     p.wmask = wmask;
     p.fuse_merge = fused ? 1 : 0;
+    p.fuse_slot = fused ? (int)(ix->fuse_seq++ % kFuseSlots) : 0;
     p.mp = mp;
     e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, p, pl.grid, pl.smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "scan launch");

@@ -11,13 +11,16 @@
 namespace linr {
 
 constexpr int kHdrBytes = 256;   // device header at the start of live_storage
+constexpr int kFuseSlots = 16;   // searches of one index that may be in flight at once (any streams)
 struct DevHeader {               // lives in device memory
   unsigned long long hwm;        // local rows [0, hwm) may be live
   unsigned long long skipped;    // out-of-shard ids seen by update/delete
   unsigned long long overflow;   // scan buffer overflows (must stay 0; checked by tests)
-  unsigned int done_ctas;        // scan CTAs finished (fused merge ticket; self-resetting)
-  unsigned int merged;           // users merged by the fused tail (self-resetting)
+  // fused-merge tickets, one slot per in-flight search (searches may overlap across streams):
+  unsigned int done_ctas[kFuseSlots];   // scan CTAs finished (self-resetting)
+  unsigned int merged[kFuseSlots];      // users merged by the fused tail (self-resetting)
 };
+static_assert(sizeof(DevHeader) <= kHdrBytes, "device header too large");
 
 struct KClause {                 // clause as the kernels see it (16 B)
   unsigned long long mask;
@@ -69,6 +72,7 @@ struct ScanParams {
   int* out_cnt;                  // [nu][gridDim.x] keys in out_list
   int64_t* out_pass;             // [nu][gridDim.x]
   unsigned long long* dbg;        // diagnostics timers (null unless linr_debug_timers(1))
+  int fuse_slot;          // DevHeader ticket slot of this search
   int fuse_merge;                // 1: the last nu CTAs run the merge (mp) for this launch's users
   MergeParams mp;                // merge of this launch's users (user index relative to the launch)
   int ncl[8];

@@ -672,22 +672,22 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   if (!p.fuse_merge) return;
   __threadfence();   // this CTA's outputs are visible before it takes a ticket
   __syncthreads();
-  if (tid == 0) ctl->ticket = (int)atomicAdd(&p.hdr->done_ctas, 1u);
+  if (tid == 0) ctl->ticket = (int)atomicAdd(&p.hdr->done_ctas[p.fuse_slot], 1u);
   __syncthreads();
   const int ticket = ctl->ticket;
   const int first = (int)gridDim.x - p.nu;
   if (ticket < first) return;
   if (tid == 0) {   // wait until every CTA of this launch has published its outputs
-    while (*(volatile unsigned int*)&p.hdr->done_ctas < gridDim.x) __nanosleep(64);
+    while (*(volatile unsigned int*)&p.hdr->done_ctas[p.fuse_slot] < gridDim.x) __nanosleep(64);
   }
   __syncthreads();
   __threadfence();
   merge_user<NT>(p.mp, ticket - first, smem_raw);
   if (tid == 0) {
-    if (atomicAdd(&p.hdr->merged, 1u) == (unsigned int)p.nu - 1) {   // last merger resets the counters
-      p.hdr->merged = 0u;
+    if (atomicAdd(&p.hdr->merged[p.fuse_slot], 1u) == (unsigned int)p.nu - 1) {   // last merger resets the slot
+      p.hdr->merged[p.fuse_slot] = 0u;
       __threadfence();
-      atomicExch(&p.hdr->done_ctas, 0u);
+      atomicExch(&p.hdr->done_ctas[p.fuse_slot], 0u);
     }
   }
 }

@@ -288,6 +288,26 @@ LINR_DEV bool tc_clauses(const uint4* k, int maxc, const unsigned char* ad, int 
   return ok;
 }
 
+// Same, with the row's word 0 in a register when it is the only word clauses read (one = true).
+LINR_DEV bool tc_clauses_reg(const uint4* k, int maxc, uint64_t w0, bool one, const unsigned char* ad, int arow) {
+  if (!one) return tc_clauses(k, maxc, ad, arow);
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c < maxc) {
+      const uint4 kr = k[c];
+      const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
+      ok = ok && (((w0 & mask) != 0ull) != (kr.w != 0u));
+    }
+  }
+  for (int c = 4; c < maxc; ++c) {
+    const uint4 kr = k[c];
+    const uint64_t mask = ((uint64_t)kr.y << 32) | kr.x;
+    ok = ok && (((w0 & mask) != 0ull) != (kr.w != 0u));
+  }
+  return ok;
+}
+
 // One CTA per SM, persistent over its tiles. Warp 0: TMA producer (item tile + attribute/live
 // stage per tile, queries once). Warp 1: MMA issuer (NKS K-steps over the tile, plus, for the
 // float kinds in the main pass, one extra K-step that adds -t_u to every column of user u so the
@@ -522,6 +542,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       const uint32_t lw = reinterpret_cast<const uint32_t*>(ad + L.live)[row >> 5];
       const bool live = ((lw >> (row & 31)) & 1u) && (t * kTcRows + row < hwm);
       const uint32_t rbase = p.row0 + (uint32_t)(t * kTcRows) + (uint32_t)((warp & 3) * 32);
+      const bool aw = p.wmax == 1;   // single attribute word: keep this row's word in registers
+      const uint64_t aw0 = p.wmax >= 1 ? reinterpret_cast<const uint64_t*>(ad)[row] : 0ull;
       for (int ch = grp; ch < nchunks; ch += NGRP) {
         uint32_t v[CW];
         tmem_ld<CW>(tmem + lane_base + (uint32_t)(acc * NP + ch * CW), v);
@@ -545,15 +567,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           }
         }
         if (sample) {
-          // ---- sample pass: thread per row, every passing user of the chunk
-          if (live) {
+          // ---- sample pass: thread per row; per user of the chunk (warp-uniform), the passing rows
+          // append with one shared-memory atomic per warp
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-              if ((j & (V - 1)) != 0 || c0 + j >= p.nvec) continue;
-              const int u = (c0 + j) >> lv;
-              if (!tc_clauses(sCl + u * p.maxc, p.maxc, ad, row)) continue;
+          for (int j = 0; j < CW; ++j) {
+            if ((j & (V - 1)) != 0 || c0 + j >= p.nvec) continue;
+            const int u = (c0 + j) >> lv;
+            const bool ok = live && tc_clauses_reg(sCl + u * p.maxc, p.maxc, aw0, aw, ad, row);
+            const uint32_t m = __ballot_sync(0xffffffffu, ok);
+            if (m == 0u) continue;
+            const int leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&sCnt[u], __popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (ok) {
+              const int pos = base + __popc(m & lanemask_lt());
               const float sj = kInt ? (float)(int)v[j] : __uint_as_float(v[j]);
-              const int pos = atomicAdd(&sCnt[u], 1);
               if (pos < p.cap) p.buf[((size_t)u * gridDim.x + blockIdx.x) * p.cap + pos] = make_key(sj, rbase + lane);
             }
           }
@@ -612,6 +641,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           for (int k = 0; bb; ++k) {
             const int r = __ffs(bb) - 1;
             bb &= bb - 1u;
+            const uint64_t w0r = __shfl_sync(0xffffffffu, aw0, r);   // row r's attribute word 0
             if (!lead) continue;
             const uint32_t raw = scr[k * kTcScrStride + lane];
             float sj;
@@ -629,7 +659,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
             }
             if (q) {
               const uint64_t key = make_key(sj, rbase + (uint32_t)r);
-              if (key >= sThr[uj] && tc_clauses(sCl + uj * p.maxc, p.maxc, ad, (warp & 3) * 32 + r)) {
+              if (key >= sThr[uj] && tc_clauses_reg(sCl + uj * p.maxc, p.maxc, w0r, aw, ad, (warp & 3) * 32 + r)) {
                 const int pos = atomicAdd(&sCnt[uj], 1);
                 if (pos < p.cap) p.buf[((size_t)uj * gridDim.x + blockIdx.x) * p.cap + pos] = key;
               }

@@ -220,6 +220,13 @@ class Index:
             self._ws[key] = ws
         return ws
 
+    def new_workspace(self, B: int, V: int, K: int) -> torch.Tensor:
+        """A private search workspace (for searches overlapping on other streams)."""
+        n = library().linr_search_workspace_bytes(self._h, B, V, K)
+        if n == 0:
+            raise LinrError(-1, f"no workspace for B={B} V={V} K={K}")
+        return torch.empty(n, dtype=torch.uint8, device=self.device)
+
     def _q(self, queries: torch.Tensor):
         q = queries
         if q.dim() == 2:
@@ -227,10 +234,11 @@ class Index:
         assert q.dtype == TORCH_DTYPE[self.dtype] and q.shape[-1] == self.dim and q.device == self.device
         return q.contiguous()
 
-    def search(self, queries: torch.Tensor, clauses, K: int, out=None, want_pass: bool = True):
+    def search(self, queries: torch.Tensor, clauses, K: int, out=None, want_pass: bool = True, ws=None):
         """Filtered top-K. queries [B][d] or [B][V][d] (index dtype, on device); clauses: per-query
         lists of (mask, word, reverse) or a Clauses object. Returns (ids [B][K] int64,
-        scores [B][K] fp32, pass [B] int64) on the device."""
+        scores [B][K] fp32, pass [B] int64) on the device. Runs on the current torch stream; searches
+        in flight on different streams need their own workspace (ws = self.new_workspace(...))."""
         q = self._q(queries)
         B, V, _ = q.shape
         cl = clause_array(clauses)
@@ -241,7 +249,8 @@ class Index:
             ps = torch.empty(B, dtype=torch.int64, device=self.device)
         else:
             ids, sc, ps = out
-        ws = self.workspace(B, V, K)
+        if ws is None:
+            ws = self.workspace(B, V, K)
         _check(library().linr_search(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
                                      ws.numel(), ids.data_ptr(), sc.data_ptr(),
                                      ps.data_ptr() if want_pass else None, _stream(self.device)))

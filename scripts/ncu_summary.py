@@ -1,8 +1,9 @@
 """Summarise ncu outputs into profiles/: a launch-list share table and per-kernel key metrics.
 
-usage: python scripts/ncu_summary.py <tag> [--launches gpurun_out/launches.csv] [--rep gpurun_out/x.ncu-rep ...]
-Writes profiles/<tag>_launches.md, profiles/<tag>_<rep-stem>.md and, for the scan kernel,
-profiles/scan_traffic.json (dram bytes per launch, read by bench.py's roofline.traffic).
+usage: python scripts/ncu_summary.py <tag> [--launches gpurun_out/launches.csv] [--rep x.ncu-rep ...]
+                                     [--workload "<bench config.workload>"]
+Writes profiles/<tag>_launches.md, profiles/<tag>_<rep-stem>.md and, with --workload,
+profiles/scan_traffic.json[workload] (dram bytes per launch, read by bench.py's roofline.traffic).
 """
 import argparse
 import collections
@@ -52,7 +53,7 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "smsp__inst_executed_pipe_tensor", "sm__inst_executed_pipe_tensor"]
 
 
-def report(rep, tag):
+def report(rep, tag, workload=None):
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(det)))
     h = r[0]
@@ -101,13 +102,15 @@ def report(rep, tag):
     print(p)
     rd = vals.get("dram__bytes_read.sum", (None, None))
     wr = vals.get("dram__bytes_write.sum", (None, None))
-    if "scan_gemv" in kern and rd[0] is not None:
+    if workload and rd[0] is not None:
         def to_bytes(v, u):
             v = float(v.replace(",", ""))
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         tb = to_bytes(*rd) + to_bytes(*wr)
-        json.dump({"kernel": kern, "dram_bytes_per_launch": tb, "source": os.path.relpath(p, ROOT)},
-                  open(os.path.join(PROF, "scan_traffic.json"), "w"), indent=1)
+        jp = os.path.join(PROF, "scan_traffic.json")
+        db = json.load(open(jp)) if os.path.exists(jp) else {}
+        db[workload] = {"kernel": kern, "dram_bytes_per_launch": tb, "source": os.path.relpath(p, ROOT)}
+        json.dump(db, open(jp, "w"), indent=1)
 
 
 if __name__ == "__main__":
@@ -115,9 +118,10 @@ if __name__ == "__main__":
     ap.add_argument("tag")
     ap.add_argument("--launches")
     ap.add_argument("--rep", nargs="*", default=[])
+    ap.add_argument("--workload", default=None, help="bench workload name: record dram bytes in scan_traffic.json")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.tag)
     for rep in a.rep:
-        report(rep, a.tag)
+        report(rep, a.tag, a.workload)

@@ -20,6 +20,7 @@ ap.add_argument("--V", type=int, default=1)
 ap.add_argument("--K", type=int, default=1000)
 ap.add_argument("--preset", default="HIGH")
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--no-pass", action="store_true", help="no pass counts (the bench configuration for B > 8)")
 a = ap.parse_args()
 dt = dg.DTYPE_NAMES[a.dtype]
 ix = Index(a.items, a.dim, dt, 1)
@@ -33,6 +34,6 @@ else:
 cls = Clauses(dg.gen_clauses(dg.QUERY_SEED, a.batch, a.preset))
 torch.cuda.synchronize()
 for _ in range(a.iters):
-    r = ix.search(q, cls, a.K)
+    r = ix.search(q, cls, a.K, want_pass=not a.no_pass)
 torch.cuda.synchronize()
 print("pass", r[2].tolist()[:4], "top", r[1][0, :3].tolist())

@@ -212,6 +212,31 @@ def test_search_host_e2e_path():
     check(dg.BF16, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what="host")
 
 
+def test_concurrent_searches_on_streams():
+    """Searches of one index in flight on several streams (own workspaces; the fused merge's
+    per-search ticket slots) give the same results as the oracle, for many interleaved calls."""
+    n, d, K = 120_000, 128, 200
+    vals, attrs = dg.gen_items(3, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    presets = ["HIGH", "LOW", "ALL", "HIGH4"]
+    Qs = [dg.gen_queries(10 + i, 3, n, 1, 1, d, dg.BF16, dg.MODE_GRID) for i in range(4)]
+    cls = [dg.gen_clauses(10 + i, 1, presets[i]) for i in range(4)]
+    qd = [to_torch(Q, dg.BF16, DEV) for Q in Qs]
+    streams = [torch.cuda.Stream(DEV) for _ in range(3)]
+    wss = [ix.new_workspace(1, 1, K) for _ in range(3)]
+    outs = []
+    torch.cuda.synchronize()
+    for k in range(24):
+        j, i = k % 3, k % 4
+        with torch.cuda.stream(streams[j]):
+            outs.append((i, ix.search(qd[i], cls[i], K, ws=wss[j])))
+            outs[-1] = (i, tuple(t.clone() for t in outs[-1][1]))   # snapshot before the stream reuses ws
+    torch.cuda.synchronize()
+    refs = [oracle.search(dg.BF16, vals, attrs, np.ones(n), Qs[i], cls[i], K) for i in range(4)]
+    for k, (i, g) in enumerate(outs):
+        check(dg.BF16, vals, attrs, np.ones(n), Qs[i], cls[i], K, g, refs[i], True, what=f"stream call {k}")
+
+
 def test_invalid_arguments_raise():
     from paper_2407_13218_b200 import Index, LinrError
     ix = Index(1000, 64, dg.I8, 1)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -127,6 +128,7 @@ struct Plan {
   int nt = 0;
   int C = 0, bufcap = 0;
   int list_cap = 0;   // per-CTA output list capacity
+  int ring = 0;       // > 0: warp-specialised scan with this many row-group slots
   size_t smem = 0;
   int grid = 0;
 };
@@ -142,6 +144,39 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
     const ScanCfg cfg = scan_gemv_cfg(dt, dim, nqv);
     if (cfg.nt == 0) continue;
     const int nw = cfg.nt / 32;
+    if (cfg.ws_slot_bytes > 0 && !std::getenv("LINR_NO_WS")) {
+      // ring scan (scan_ws.cuh): R (a power of two) slots of 16 rows, ~128 KB of rows in flight
+      // by default; the rest of shared memory for the per-user key buffers (>= K + 256 keys)
+      const int head = cfg.ws_cons_warps * 16;
+      const size_t rows_b = (size_t)cfg.ws_slot_bytes - 96;
+      const char* rk = std::getenv("LINR_WS_RING_KB");   // tuning knob (KB of rows in the ring)
+      const size_t ring_target = (rk ? (size_t)std::atoi(rk) : 128) * 1024;
+      int R = 8;
+      while (R < 64 && (size_t)(2 * R) * rows_b <= ring_target) R *= 2;
+      long long C = 0;
+      for (; R >= 8; R /= 2) {
+        const size_t fixed = (size_t)cfg.ws_fixed_bytes + (size_t)R * cfg.ws_slot_bytes;
+        if (ix->smem_optin <= fixed) continue;
+        C = (long long)((ix->smem_optin - fixed) / (8 * (size_t)nu)) - head;
+        C = std::min<long long>(C, 32768);
+        C &= ~255ll;
+        if (C >= K + 256) break;
+      }
+      if (R >= 8) {
+        pl->nu_g = nu;
+        pl->groups = (B + nu - 1) / nu;
+        pl->nqv = nqv;
+        pl->nt = cfg.nt;
+        pl->C = (int)C;
+        pl->bufcap = (int)C + head;
+        pl->ring = R;
+        pl->smem = std::max((size_t)cfg.ws_fixed_bytes + (size_t)R * cfg.ws_slot_bytes + (size_t)nu * pl->bufcap * 8,
+                            merge_smem());
+        pl->grid = (pl->groups == 1 && ix->num_sms > 1) ? ix->num_sms - 1 : ix->num_sms;
+        pl->list_cap = (B <= 8) ? pl->bufcap : std::min(pl->bufcap, std::max(2 * K, 2048));
+        return true;
+      }
+    }
     const int head = nw * cfg.rows_per_iter;
     const size_t fixed = kScanCtlBytes + (size_t)nw * kTileItems * 2 + (size_t)nw * cfg.ring_bytes;
     if (ix->smem_optin <= fixed) continue;
@@ -481,6 +516,7 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
     }
     p.wmask = wmask;
     p.fuse_merge = fused ? 1 : 0;
+    p.ring = pl.ring;
     p.fuse_slot = fused ? (int)(ix->fuse_seq++ % kFuseSlots) : 0;
     p.mp = mp;
     e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, p, pl.grid, pl.smem, st);

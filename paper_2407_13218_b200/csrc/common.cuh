@@ -44,6 +44,11 @@ LINR_DEV uint4 ldg_stream_v4(const void* p) {
                : "l"(p));
   return r;
 }
+LINR_DEV uint32_t ldg_stream_u32(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 LINR_DEV uint64_t ldg_stream_u64(const uint64_t* p) {
   uint64_t r;
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(r) : "l"(p));
@@ -62,6 +67,17 @@ LINR_DEV void dbg_mark(unsigned long long* d, int slot) {
 }
 
 // ---------------------------------------------------------------- CTA-wide primitives
+// Barrier of the NT threads taking part in a CTA-wide primitive: BAR = 0 is the whole CTA
+// (__syncthreads), BAR > 0 a named barrier over NT threads (a role subset of a warp-specialised CTA).
+template <int BAR, int NT>
+LINR_DEV void part_sync() {
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  }
+}
+
 // Scratch used by the CTA-wide helpers (lives in shared memory).
 struct SelScratch {
   int hist[256];
@@ -76,9 +92,9 @@ struct SelScratch {
 // differ (so the first digit already spreads the keys); stops early once the selected digit's
 // whole bucket belongs to the top-k. Plain shared-memory atomics for the histogram: measured on
 // B200 2.4x faster than warp-aggregating them with __match_any_sync.
-template <int NT, typename Get>
-__device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <int NT, int BAR = 0, typename Get>
+__device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc, int tid = threadIdx.x) {
+  const int lane = tid & 31, warp = tid >> 5;
   unsigned long long a = ~0ull, o = 0ull;
   for (int i = tid; i < n; i += NT) {
     uint64_t v = get(i);
@@ -90,12 +106,12 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
     o |= __shfl_xor_sync(0xffffffffu, o, off);
   }
   if (tid == 0) { sc->red_and = ~0ull; sc->red_or = 0ull; }
-  __syncthreads();
+  part_sync<BAR, NT>();
   if (lane == 0) { atomicAnd(&sc->red_and, a); atomicOr(&sc->red_or, o); }
-  __syncthreads();
+  part_sync<BAR, NT>();
   const unsigned long long diff = sc->red_and ^ sc->red_or;
   const unsigned long long orv = sc->red_or;
-  __syncthreads();
+  part_sync<BAR, NT>();
   if (diff == 0ull) return orv;   // n == 1 (distinct keys): the key itself
   const int hb = 63 - __clzll((long long)diff);
   uint64_t pmask = (hb == 63) ? 0ull : (~0ull << (hb + 1));
@@ -104,12 +120,12 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
   int kk = k;
   while (true) {
     for (int i = tid; i < 256; i += NT) sc->hist[i] = 0;
-    __syncthreads();
+    part_sync<BAR, NT>();
     for (int i = tid; i < n; i += NT) {
       const uint64_t v = get(i);
       if ((v & pmask) == prefix) atomicAdd(&sc->hist[(int)((v >> shift) & 255u)], 1);
     }
-    __syncthreads();
+    part_sync<BAR, NT>();
     if (warp == 0) {
       int c[8], s = 0;
 #pragma unroll
@@ -138,9 +154,9 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
         }
       }
     }
-    __syncthreads();
+    part_sync<BAR, NT>();
     const int d = sc->sel_digit, above = sc->sel_above, cnt = sc->sel_cnt;
-    __syncthreads();
+    part_sync<BAR, NT>();
     prefix = (prefix & ~(0xFFull << shift)) | ((uint64_t)d << shift);
     pmask |= 0xFFull << shift;
     kk -= above;
@@ -152,9 +168,9 @@ __device__ uint64_t block_select_ge(Get get, int n, int k, SelScratch* sc) {
 
 // In-place, order-preserving compaction of buf[0..n) to the keys >= T. Returns the new count.
 // Two barriers per NT-key chunk; warp 0 scans the per-warp counts.
-template <int NT>
-__device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <int NT, int BAR = 0>
+__device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc, int tid = threadIdx.x) {
+  const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   int running = 0;
   for (int base = 0; base < n; base += NT) {
@@ -163,7 +179,7 @@ __device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc
     const bool keep = (i < n) && v >= T;
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) sc->warp_cnt[warp] = __popc(bal);
-    __syncthreads();   // all reads of this chunk done, warp counts visible
+    part_sync<BAR, NT>();   // all reads of this chunk done, warp counts visible
     if (warp == 0) {
       const int c = lane < NW ? sc->warp_cnt[lane] : 0;
       int incl = c;
@@ -175,11 +191,11 @@ __device__ int block_compact_ge(uint64_t* buf, int n, uint64_t T, SelScratch* sc
       if (lane < NW) sc->hist[lane] = incl - c;   // exclusive warp offsets
       if (lane == 31) sc->total = incl;
     }
-    __syncthreads();
+    part_sync<BAR, NT>();
     if (keep) buf[running + sc->hist[warp] + __popc(bal & lanemask_lt())] = v;
     running += sc->total;
   }
-  __syncthreads();
+  part_sync<BAR, NT>();
   return running;
 }
 

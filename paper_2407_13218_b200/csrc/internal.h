@@ -74,6 +74,7 @@ struct ScanParams {
   unsigned long long* dbg;        // diagnostics timers (null unless linr_debug_timers(1))
   int fuse_slot;          // DevHeader ticket slot of this search
   int fuse_merge;                // 1: the last nu CTAs run the merge (mp) for this launch's users
+  int ring;                      // > 0: warp-specialised scan with this many row-group slots
   MergeParams mp;                // merge of this launch's users (user index relative to the launch)
   int ncl[8];
   KClause cl[8][16];
@@ -83,6 +84,9 @@ struct ScanCfg {                 // launch geometry chosen for one (dtype, dim, 
   int nt;                        // threads per CTA
   int rows_per_iter;             // rows a warp scores per inner iteration (append burst bound)
   int ring_bytes;                // per-warp cp.async row ring (stages x rows_per_iter x row bytes)
+  int ws_slot_bytes;             // > 0: warp-specialised kernel available; bytes per row-group slot
+  int ws_fixed_bytes;            // its shared memory besides the slots and the key buffers
+  int ws_cons_warps;             // its warps that append keys (buffer headroom: 16 keys each)
 };
 constexpr int kScanSample = 32;  // sorted per-CTA sample length
 

@@ -140,6 +140,11 @@ struct ScanCtl {
   int next_tile;                       // CTA-local dynamic tile counter
   int wcnt;                            // write counter for the final list
   int ticket;                          // fused-merge ticket of this CTA
+  // warp-specialised scan (scan_ws_kernel): row-group ring bookkeeping
+  int ghead;                           // row groups allocated by the producer warps
+  int gtotal;                          // total groups, published when every producer is done
+  int pdone;                           // warps finished filtering
+  int gcons;                           // row groups claimed by scoring warps
 };
 
 static_assert(sizeof(ScanCtl) + 16 <= 2048, "host plan reserves 2 KB for ScanCtl (api.cu kScanCtlBytes)");
@@ -269,6 +274,81 @@ struct ScanGeom {
   static constexpr int RING = kMma ? MmaGeom<DT, D>::S * MmaGeom<DT, D>::STAGE
                                    : kStages * RowGeom<DT, D, NQV>::RPI * RowGeom<DT, D, NQV>::ROWB;
 };
+
+// Per-CTA output (sorted top-32 sample + every kept key) and the fused merge, run by all NT
+// threads of the CTA once the scan of its range is complete. rings: >= 512 idle bytes (scratch).
+template <int NT>
+__device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const ScanParams& p, unsigned char* rings,
+                                          unsigned char* smem_raw) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- 4. per-CTA output: sorted top-32 sample + the whole (unsorted) buffer
+  uint64_t* scratch64 = reinterpret_cast<uint64_t*>(rings);   // 64 keys (the rings are idle now)
+  const size_t cta = (size_t)blockIdx.x;
+  for (int u = 0; u < p.nu; ++u) {
+    uint64_t* b = bufs + (size_t)u * p.bufcap;
+    int n = min(ctl->count[u], p.bufcap);
+    if (n > p.list_cap) {
+      const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, p.K, &ctl->sel);
+      n = block_compact_ge<NT>(b, n, T, &ctl->sel);
+    }
+    // sample: the top-32 keys, sorted
+    if (n > kSample) {
+      const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
+      if (tid == 0) ctl->wcnt = 0;
+      __syncthreads();
+      for (int i0 = 0; i0 < n; i0 += NT) {
+        const int i = i0 + tid;
+        const bool top = i < n && b[i] >= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, top);
+        int at = 0;
+        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (top) scratch64[at + __popc(bal & lanemask_lt())] = b[i];
+      }
+      __syncthreads();
+    } else {
+      for (int i = tid; i < kSample; i += NT) scratch64[i] = i < n ? b[i] : 0ull;
+      __syncthreads();
+    }
+    uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
+    if (warp == 0) {
+      scratch64[32 + lane] = 0ull;
+      __syncwarp();
+      warp_sort64_desc(scratch64);
+      samp[lane] = scratch64[lane];
+    }
+    uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;
+    for (int i = tid; i < n; i += NT) lst[i] = b[i];
+    if (tid == 0) p.out_cnt[(size_t)u * gridDim.x + cta] = n;
+    __syncthreads();
+  }
+  if (tid < p.nu) p.out_pass[(size_t)tid * gridDim.x + cta] = (int64_t)ctl->pass[tid];
+  if (tid == 0 && ctl->overflow) atomicAdd(&p.hdr->overflow, (unsigned long long)ctl->overflow);
+  dbg_mark(p.dbg, blockIdx.x * 8 + 3);
+
+  // ---- 5. fused merge: the last nu CTAs to finish merge one user each (no extra launch)
+  if (!p.fuse_merge) return;
+  __threadfence();   // this CTA's outputs are visible before it takes a ticket
+  __syncthreads();
+  if (tid == 0) ctl->ticket = (int)atomicAdd(&p.hdr->done_ctas[p.fuse_slot], 1u);
+  __syncthreads();
+  const int ticket = ctl->ticket;
+  const int first = (int)gridDim.x - p.nu;
+  if (ticket < first) return;
+  if (tid == 0) {   // wait until every CTA of this launch has published its outputs
+    while (*(volatile unsigned int*)&p.hdr->done_ctas[p.fuse_slot] < gridDim.x) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  merge_user<NT>(p.mp, ticket - first, smem_raw);
+  if (tid == 0) {
+    if (atomicAdd(&p.hdr->merged[p.fuse_slot], 1u) == (unsigned int)p.nu - 1) {   // last merger resets the slot
+      p.hdr->merged[p.fuse_slot] = 0u;
+      __threadfence();
+      atomicExch(&p.hdr->done_ctas[p.fuse_slot], 0u);
+    }
+  }
+}
 
 template <int DT, int D, int NQV, int NT>
 __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant__ ScanParams p) {
@@ -623,145 +703,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   __syncthreads();
   dbg_mark(p.dbg, blockIdx.x * 8 + 1);
 
-  // ---- 4. per-CTA output: sorted top-32 sample + the whole (unsorted) buffer
-  uint64_t* scratch64 = reinterpret_cast<uint64_t*>(rings);   // 64 keys (the rings are idle now)
-  const size_t cta = (size_t)blockIdx.x;
-  for (int u = 0; u < p.nu; ++u) {
-    uint64_t* b = bufs + (size_t)u * p.bufcap;
-    int n = min(ctl->count[u], p.bufcap);
-    if (n > p.list_cap) {
-      const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, p.K, &ctl->sel);
-      n = block_compact_ge<NT>(b, n, T, &ctl->sel);
-    }
-    // sample: the top-32 keys, sorted
-    if (n > kSample) {
-      const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
-      if (tid == 0) ctl->wcnt = 0;
-      __syncthreads();
-      for (int i0 = 0; i0 < n; i0 += NT) {
-        const int i = i0 + tid;
-        const bool top = i < n && b[i] >= T;
-        const uint32_t bal = __ballot_sync(0xffffffffu, top);
-        int at = 0;
-        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
-        at = __shfl_sync(0xffffffffu, at, 0);
-        if (top) scratch64[at + __popc(bal & lanemask_lt())] = b[i];
-      }
-      __syncthreads();
-    } else {
-      for (int i = tid; i < kSample; i += NT) scratch64[i] = i < n ? b[i] : 0ull;
-      __syncthreads();
-    }
-    uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
-    if (warp == 0) {
-      scratch64[32 + lane] = 0ull;
-      __syncwarp();
-      warp_sort64_desc(scratch64);
-      samp[lane] = scratch64[lane];
-    }
-    uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;
-    for (int i = tid; i < n; i += NT) lst[i] = b[i];
-    if (tid == 0) p.out_cnt[(size_t)u * gridDim.x + cta] = n;
-    __syncthreads();
-  }
-  if (tid < p.nu) p.out_pass[(size_t)tid * gridDim.x + cta] = (int64_t)ctl->pass[tid];
-  if (tid == 0 && ctl->overflow) atomicAdd(&p.hdr->overflow, (unsigned long long)ctl->overflow);
-  dbg_mark(p.dbg, blockIdx.x * 8 + 3);
-
-  // ---- 5. fused merge: the last nu CTAs to finish merge one user each (no extra launch)
-  if (!p.fuse_merge) return;
-  __threadfence();   // this CTA's outputs are visible before it takes a ticket
-  __syncthreads();
-  if (tid == 0) ctl->ticket = (int)atomicAdd(&p.hdr->done_ctas[p.fuse_slot], 1u);
-  __syncthreads();
-  const int ticket = ctl->ticket;
-  const int first = (int)gridDim.x - p.nu;
-  if (ticket < first) return;
-  if (tid == 0) {   // wait until every CTA of this launch has published its outputs
-    while (*(volatile unsigned int*)&p.hdr->done_ctas[p.fuse_slot] < gridDim.x) __nanosleep(64);
-  }
-  __syncthreads();
-  __threadfence();
-  merge_user<NT>(p.mp, ticket - first, smem_raw);
-  if (tid == 0) {
-    if (atomicAdd(&p.hdr->merged[p.fuse_slot], 1u) == (unsigned int)p.nu - 1) {   // last merger resets the slot
-      p.hdr->merged[p.fuse_slot] = 0u;
-      __threadfence();
-      atomicExch(&p.hdr->done_ctas[p.fuse_slot], 0u);
-    }
-  }
+  scan_tail<NT>(ctl, bufs, p, rings, smem_raw);
 }
-
-template <int DT>
-struct ScanDispatch {
-  template <int D, int NQV>
-  static constexpr int nt() {
-    return 512;   // 16 warps x 128 registers: query chunks + next-tile prefetch stay in registers
-  }
-  template <int D, int NQV>
-  static cudaError_t go(const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
-    constexpr int NT = nt<D, NQV>();
-    auto k = scan_gemv_kernel<DT, D, NQV, NT>;
-    static size_t smem_set = 0;   // opt-in size already granted to this instance
-    if (smem > smem_set) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      smem_set = smem;
-    }
-    // grid = #SMs at one CTA per SM: every CTA is resident, so the fused merge's wait for the
-    // other CTAs of the launch cannot deadlock (CTAs only wait on CTAs of the same launch).
-    k<<<grid, NT, smem, st>>>(p);
-    return cudaGetLastError();
-  }
-  template <int D>
-  static cudaError_t by_nqv(int nqv, const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
-    switch (nqv) {
-      case 1: return go<D, 1>(p, grid, smem, st);
-      case 2: return go<D, 2>(p, grid, smem, st);
-      case 4: return go<D, 4>(p, grid, smem, st);
-      case 8: return go<D, 8>(p, grid, smem, st);
-    }
-    return cudaErrorInvalidValue;
-  }
-  static cudaError_t launch(int dim, int nqv, const ScanParams& p, int grid, size_t smem, cudaStream_t st) {
-    switch (dim) {
-      case 16: return by_nqv<16>(nqv, p, grid, smem, st);
-      case 32: return by_nqv<32>(nqv, p, grid, smem, st);
-      case 64: return by_nqv<64>(nqv, p, grid, smem, st);
-      case 128: return by_nqv<128>(nqv, p, grid, smem, st);
-      case 256: return by_nqv<256>(nqv, p, grid, smem, st);
-      case 512: return by_nqv<512>(nqv, p, grid, smem, st);
-      case 1024: return by_nqv<1024>(nqv, p, grid, smem, st);
-    }
-    return cudaErrorInvalidValue;
-  }
-  template <int D, int NQV>
-  static ScanCfg cfg_dq() {
-    using SG = ScanGeom<DT, D, NQV>;
-    return ScanCfg{nt<D, NQV>(), SG::RPI, SG::RING};
-  }
-  template <int D>
-  static ScanCfg cfg_d(int nqv) {
-    switch (nqv) {
-      case 1: return cfg_dq<D, 1>();
-      case 2: return cfg_dq<D, 2>();
-      case 4: return cfg_dq<D, 4>();
-      case 8: return cfg_dq<D, 8>();
-    }
-    return ScanCfg{0, 0, 0};
-  }
-  static ScanCfg cfg(int dim, int nqv) {
-    switch (dim) {
-      case 16: return cfg_d<16>(nqv);
-      case 32: return cfg_d<32>(nqv);
-      case 64: return cfg_d<64>(nqv);
-      case 128: return cfg_d<128>(nqv);
-      case 256: return cfg_d<256>(nqv);
-      case 512: return cfg_d<512>(nqv);
-      case 1024: return cfg_d<1024>(nqv);
-    }
-    return ScanCfg{0, 0, 0};
-  }
-};
 
 }  // namespace linr

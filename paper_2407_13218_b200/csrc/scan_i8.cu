@@ -1,5 +1,5 @@
 // Explicit instantiation of the GEMV scan kernels for dtype LINR_I8 (split per dtype for parallel builds).
-#include "scan_gemv.cuh"
+#include "scan_dispatch.cuh"
 
 namespace linr {
 cudaError_t launch_scan_gemv_i8(int dim, int nqv, const ScanParams& p, int grid, size_t smem, cudaStream_t st) {

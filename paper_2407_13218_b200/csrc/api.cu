@@ -158,7 +158,10 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
         const size_t fixed = (size_t)cfg.ws_fixed_bytes + (size_t)R * cfg.ws_slot_bytes;
         if (ix->smem_optin <= fixed) continue;
         C = (long long)((ix->smem_optin - fixed) / (8 * (size_t)nu)) - head;
-        C = std::min<long long>(C, 32768);
+        // a smaller buffer raises the CTA's threshold earlier (compactions stall only the scoring
+        // warps, the producers keep the ring busy) and leaves fewer keys for the tail to select
+        const char* cm = std::getenv("LINR_WS_CMAX");
+        C = std::min<long long>(C, std::max<long long>(cm ? std::atoll(cm) : 32768, K + 256));
         C &= ~255ll;
         if (C >= K + 256) break;
       }
@@ -477,7 +480,11 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   mp.mode = mode;
   mp.dbg = debug_buffer();
   // one scan launch: its last CTAs run the merge (saves a launch); several: a merge kernel
-  const bool fused = pl.groups == 1;
+  // LINR_FUSE_MERGE=1: the last CTAs of a single scan launch run the merge (saves a launch, but the
+  // scan kernel then also carries the merge's latency); default: a separate merge kernel, which
+  // overlaps the next search's scan when searches are pipelined on two streams
+  static const bool fuse_env = std::getenv("LINR_FUSE_MERGE") && std::atoi(std::getenv("LINR_FUSE_MERGE")) != 0;
+  const bool fused = pl.groups == 1 && fuse_env;
   for (int g = 0; g < pl.groups; ++g) {
     const int u0 = g * pl.nu_g;
     const int nu = std::min(pl.nu_g, B - u0);

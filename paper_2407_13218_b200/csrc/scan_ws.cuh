@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
   }
   if (tid == 0) {
     ctl->flag = 0; ctl->done = 0; ctl->overflow = 0; ctl->next_tile = 0;
-    ctl->ghead = 0; ctl->gtotal = INT_MAX; ctl->pdone = 0;
+    ctl->ghead = 0; ctl->gtotal = INT_MAX; ctl->pdone = 0; ctl->gcons = 0;
   }
   for (int s = tid; s < R; s += NT) {
     ws_bar_init(&fullb[s], 33);   // 32 cp.async arrivals + the producer's metadata arrival
@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
-      if (atomicAdd(&ctl->pdone, 1) == NPW - 1) {   // every group has been allocated
+      const int order = atomicAdd(&ctl->pdone, 1);
+      if (p.dbg != nullptr && (order == 0 || order == NPW - 1)) p.dbg[blockIdx.x * 8 + (order == 0 ? 4 : 5)] = gtimer();
+      if (order == NPW - 1) {   // every group has been allocated
         const int total = atomicAdd(&ctl->ghead, 0);
         atomicExch(&ctl->gtotal, total);
       }

@@ -1,9 +1,10 @@
-# usage: bash scripts/gpu_ws.sh -- ring-scan parity tests + A/B vs the per-warp kernel
+# usage: bash scripts/gpu_ws.sh -- ring-scan parity tests + bench presets + phase timers (bounded)
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q --timeout 300 2>&1 | tail -3
+timeout 240 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q --timeout 60 2>&1 | tail -3
+for cm in 32768 4096 2048; do
 for pre in HIGH ALL LOW; do
-  echo "RING $pre: $(timeout 300 python bench.py --no-cpu-baseline --steps 200 --preset $pre 2>&1 | tail -1 | python scripts/fmt_bench.py)"
+  echo "CMAX=$cm $pre: $(LINR_WS_CMAX=$cm timeout 60 python bench.py --no-cpu-baseline --steps 200 --preset $pre 2>&1 | tail -1 | python scripts/fmt_bench.py)"
 done
-for kb in 64 256; do
-  echo "RING ${kb}KB HIGH: $(LINR_WS_RING_KB=$kb timeout 300 python bench.py --no-cpu-baseline --steps 200 2>&1 | tail -1 | python scripts/fmt_bench.py)"
 done
+echo "FUSED HIGH: $(LINR_FUSE_MERGE=1 timeout 60 python bench.py --no-cpu-baseline --steps 200 2>&1 | tail -1 | python scripts/fmt_bench.py)"
+for cm in 32768 2048; do echo "== HIGH CMAX=$cm"; LINR_WS_CMAX=$cm timeout 60 python scripts/phase_timers.py --preset HIGH; done

@@ -38,12 +38,22 @@ L.linr_debug_read(buf.ctypes.data, 8192)
 L.linr_debug_timers(0)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 sc = buf[: nsm * 8].reshape(nsm, 8).astype(np.int64)
+used = sc[:, 0] > 0
+sc = sc[used]
 t0 = sc[:, 0].min()
-rel = (sc[:, :4] - t0) / 1e3
-print(f"scan CTAs: start spread {rel[:,0].max():.2f}us  loop-end min/med/max {rel[:,1].min():.2f}/{np.median(rel[:,1]):.2f}/{rel[:,1].max():.2f}us")
-print(f"  final select (med) {np.median(rel[:,2]-rel[:,1]):.2f}us  write list (med) {np.median(rel[:,3]-rel[:,2]):.2f}us  end max {rel[:,3].max():.2f}us")
+st = (sc[:, 0] - t0) / 1e3
+rel = lambda k: (sc[:, k] - sc[:, 0]) / 1e3
+def q(x):
+    return f"min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}"
+print(f"scan CTAs {used.sum()}: start spread {st.max():.2f} us")
+if (sc[:, 4] > 0).all():
+    print(f"  first producer done  {q(rel(4))}")
+    print(f"  last producer done   {q(rel(5))}")
+print(f"  scan loop end        {q(rel(1))}")
+print(f"  tail end             {q(rel(3))}")
+print(f"  absolute tail end (from first start) max {((sc[:, 3] - t0) / 1e3).max():.2f} us")
 print(f"  compactions per CTA: min {sc[:,7].min()} med {np.median(sc[:,7])} max {sc[:,7].max()}")
 m = buf[4096:4104].astype(np.int64)
-mr = (m[:7] - t0) / 1e3
-print("bucket maxb", int(buf[6144]) & 0xFFFFFFFF, "bucket_ok", int(buf[6144]) >> 32)
-print(f"merge: start {mr[0]:.2f}  gather-done {mr[1]-mr[0]:.2f}  lb {mr[2]-mr[1]:.2f}  prune {mr[3]-mr[2]:.2f}  select {mr[4]-mr[3]:.2f}  sort {mr[5]-mr[4]:.2f}  out {mr[6]-mr[5]:.2f}  n={m[7]}  (us)")
+if m[0] > 0:
+    mr = (m[:7] - t0) / 1e3
+    print(f"merge: start {mr[0]:.2f}  gather-done {mr[1]-mr[0]:.2f}  lb {mr[2]-mr[1]:.2f}  prune {mr[3]-mr[2]:.2f}  select {mr[4]-mr[3]:.2f}  sort {mr[5]-mr[4]:.2f}  out {mr[6]-mr[5]:.2f}  n={m[7]}  (us)")

@@ -331,7 +331,7 @@ def run_gpu(args):
     if alg_bytes is not None and scan_ms > 0:
         ach = alg_bytes / (scan_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": "scan_gemv_kernel<bf16,128,1>",
+                "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": "scan_ws_kernel<bf16,128,1> (warp-specialised ring scan; merge is a separate kernel)",
                 "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                 "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 

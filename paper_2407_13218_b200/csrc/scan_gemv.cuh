@@ -279,7 +279,7 @@ struct ScanGeom {
 // threads of the CTA once the scan of its range is complete. rings: >= 512 idle bytes (scratch).
 template <int NT>
 __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const ScanParams& p, unsigned char* rings,
-                                          unsigned char* smem_raw) {
+                                          unsigned char* smem_raw, size_t ring_bytes) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- 4. per-CTA output: sorted top-32 sample + the whole (unsorted) buffer
   uint64_t* scratch64 = reinterpret_cast<uint64_t*>(rings);   // 64 keys (the rings are idle now)
@@ -292,7 +292,8 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       n = block_compact_ge<NT>(b, n, T, &ctl->sel);
     }
     // sample: the top-32 keys, sorted
-    if (n > kSample) {
+    const int tail_cap = (int)min((size_t)1024, ring_bytes / 8 - 64);
+    if (n > kSample && tail_cap < NT) {   // no room for the candidate pass: select over the buffer
       const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
       if (tid == 0) ctl->wcnt = 0;
       __syncthreads();
@@ -304,6 +305,51 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
         if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
         at = __shfl_sync(0xffffffffu, at, 0);
         if (top) scratch64[at + __popc(bal & lanemask_lt())] = b[i];
+      }
+      __syncthreads();
+    } else if (n > kSample) {
+      // T0 = the 32nd largest of the threads' local maxima bounds the 32nd key from below (those
+      // 32 keys exist), so the top 32 are among the keys >= T0 -- usually a few dozen; collect
+      // them (cap kTailCand) and select among those. Fallback: select over the whole buffer.
+      const int kTailCand = tail_cap;
+      uint64_t* cand = scratch64 + 64;          // the rings are idle: room for kTailCand keys
+      uint64_t mx = 0ull;
+      for (int i = tid; i < n; i += NT) mx = b[i] > mx ? b[i] : mx;
+      cand[tid] = mx;
+      __syncthreads();
+      const uint64_t T0 = block_select_ge<NT>([cand](int i) { return cand[i]; }, NT, kSample, &ctl->sel);
+      if (tid == 0) ctl->wcnt = 0;
+      __syncthreads();
+      for (int i0 = 0; i0 < n; i0 += NT) {
+        const int i = i0 + tid;
+        const uint64_t v = i < n ? b[i] : 0ull;
+        const bool top = i < n && v >= T0 && v != 0ull;
+        const uint32_t bal = __ballot_sync(0xffffffffu, top);
+        int at = 0;
+        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        const int pos = at + __popc(bal & lanemask_lt());
+        if (top && pos < kTailCand) cand[pos] = v;
+      }
+      __syncthreads();
+      const int m = ctl->wcnt;
+      const bool small = m <= kTailCand;
+      uint64_t T;
+      if (small) T = m > kSample ? block_select_ge<NT>([cand](int i) { return cand[i]; }, m, kSample, &ctl->sel) : 1ull;
+      else T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
+      if (tid == 0) ctl->wcnt = 0;
+      __syncthreads();
+      const int mm = small ? m : n;
+      const uint64_t* src = small ? cand : b;
+      for (int i0 = 0; i0 < mm; i0 += NT) {
+        const int i = i0 + tid;
+        const uint64_t v = i < mm ? src[i] : 0ull;
+        const bool top = i < mm && v >= T && v != 0ull;
+        const uint32_t bal = __ballot_sync(0xffffffffu, top);
+        int at = 0;
+        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (top) scratch64[at + __popc(bal & lanemask_lt())] = v;
       }
       __syncthreads();
     } else {
@@ -703,7 +749,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   __syncthreads();
   dbg_mark(p.dbg, blockIdx.x * 8 + 1);
 
-  scan_tail<NT>(ctl, bufs, p, rings, smem_raw);
+  scan_tail<NT>(ctl, bufs, p, rings, smem_raw, (size_t)NW * RING);
 }
 
 }  // namespace linr

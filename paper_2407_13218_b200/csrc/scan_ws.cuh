@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
   for (int s = tid; s < R; s += NT) ws_bar_inval(&fullb[s]);   // the tail reuses this memory
   __syncthreads();
   dbg_mark(p.dbg, blockIdx.x * 8 + 1);
-  scan_tail<NT>(ctl, bufs, p, ring, smem_raw);
+  scan_tail<NT>(ctl, bufs, p, ring, smem_raw, (size_t)R * M::STAGE);
 }
 
 }  // namespace linr

@@ -102,7 +102,7 @@ def report(rep, tag, workload=None):
     print(p)
     rd = vals.get("dram__bytes_read.sum", (None, None))
     wr = vals.get("dram__bytes_write.sum", (None, None))
-    if workload and rd[0] is not None:
+    if workload and rd[0] is not None and "scan" in kern:
         def to_bytes(v, u):
             v = float(v.replace(",", ""))
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)

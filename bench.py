@@ -37,6 +37,7 @@ PRESET = "HIGH"
 
 
 def parse():
+    global DIM, DT, ESZ
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=500)
@@ -47,13 +48,25 @@ def parse():
     ap.add_argument("--items", type=int, default=N_ITEMS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pass-counts", action="store_true", help="batched path: also compute per-query pass counts")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f16", "i8", "f32"],
+                    help="index dtype (c2: bf16; c3/c4 shards: i8)")
+    ap.add_argument("--dim", type=int, default=DIM)
     ap.add_argument("--pipeline", type=int, default=2,
                     help="searches in flight on separate streams in the throughput region (1 = serial)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    DIM = a.dim
+    DT = {"bf16": 2, "f16": 1, "i8": 3, "f32": 0}[a.dtype]   # datagen / linr_dtype codes
+    ESZ = {"bf16": 2, "f16": 2, "i8": 1, "f32": 4}[a.dtype]
+    return a
+
+
+DT = 2     # LINR_BF16 (set from --dtype)
+ESZ = 2
 
 
 def workload_name(args, n_items):
-    return (f"c2: {n_items // 1_000_000}M items/GPU d={DIM} bf16, 64-bit attribute bitmask pre-filter "
+    tag = "c2" if (args.dtype, DIM) == ("bf16", 128) else "shard"
+    return (f"{tag}: {n_items // 1_000_000}M items/GPU d={DIM} {args.dtype}, 64-bit attribute bitmask pre-filter "
             f"({args.preset}), B={args.batch}, K={K}")
 
 
@@ -128,15 +141,15 @@ def oracle_sample(args, seconds_target=12.0, max_rows=2_000_000):
     import datagen as dg
     import oracle
     rows = min(max_rows, args.items)
-    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, dg.BF16, dg.MODE_DENSE)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, DT, dg.MODE_DENSE)
     live = np.ones(rows, np.uint8)
-    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, dg.BF16)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, DT)
     cls = dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset)
     oracle.lib()
     done_items, t_total, calls = 0, 0.0, 0
     while t_total < seconds_target or calls == 0:
         t0 = time.perf_counter()
-        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+        oracle.search(DT, vals, attrs, live, Q, cls, K)
         t_total += time.perf_counter() - t0
         done_items += rows * args.batch
         calls += 1
@@ -154,16 +167,16 @@ def run_reference(args):
     import datagen as dg
     import oracle
     rows = min(1_000_000, args.items)
-    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, dg.BF16, dg.MODE_DENSE)
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, rows, DIM, DT, dg.MODE_DENSE)
     live = np.ones(rows, np.uint8)
-    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, dg.BF16)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, args.items, args.batch, 1, DIM, DT)
     cls = dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset)
     oracle.lib()
     for _ in range(args.warmup):
-        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+        oracle.search(DT, vals, attrs, live, Q, cls, K)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.search(dg.BF16, vals, attrs, live, Q, cls, K)
+        oracle.search(DT, vals, attrs, live, Q, cls, K)
     dt = time.perf_counter() - t0
     ips = rows * args.batch * args.steps / dt
     sample = f"first {rows} rows of the {args.items}-row workload per step, B={args.batch}, single thread"
@@ -204,15 +217,18 @@ def run_gpu(args):
 
     t_build = time.perf_counter()
     if world > 1:
-        sidx = ShardedIndex(n_total, DIM, dg.BF16, 1, device=dev)
+        sidx = ShardedIndex(n_total, DIM, DT, 1, device=dev)
         sidx.generate(dg.DATA_SEED, dg.MODE_DENSE)
         ix = sidx.local
     else:
         sidx = None
-        ix = Index(n_local, DIM, dg.BF16, 1, device=dev)
+        ix = Index(n_local, DIM, DT, 1, device=dev)
         ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, n_local)
-    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n_total, args.batch, 1, DIM, dg.BF16)
-    qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16).contiguous()
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n_total, args.batch, 1, DIM, DT)
+    if DT in (dg.BF16, dg.F16):
+        qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16 if DT == dg.BF16 else torch.float16).contiguous()
+    else:
+        qh = torch.from_numpy(Q).contiguous()
     qd = qh.to(dev)
     qpin = qh.pin_memory()
     cls = Clauses(dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset))
@@ -314,7 +330,7 @@ def run_gpu(args):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    h2d = args.batch * DIM * 2
+    h2d = args.batch * DIM * ESZ
     d2h = args.batch * K * (8 + 4) + args.batch * 8
 
     items_per_step = args.batch * n_total
@@ -323,7 +339,7 @@ def run_gpu(args):
 
     # roofline of the dominant kernel (the fused scan): algorithmic bytes per launch
     # = per item 8 B attribute word + 1/8 B liveness bit, + per passing item the row (256 B)
-    rowbytes = DIM * 2
+    rowbytes = DIM * ESZ
     alg_bytes = n_local * (8 + 1 / 8) + pass_count * rowbytes if args.batch == 1 else None
     scan_ms = prof["scan_ms"] / max(1, prof["searches"])
     peak, peak_src = measured_peaks()
@@ -331,7 +347,7 @@ def run_gpu(args):
     if alg_bytes is not None and scan_ms > 0:
         ach = alg_bytes / (scan_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": "scan_ws_kernel<bf16,128,1> (warp-specialised ring scan; merge is a separate kernel)",
+                "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": f"scan_ws_kernel<{args.dtype},{DIM},1> (warp-specialised ring scan; merge is a separate kernel)",
                 "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                 "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
 
@@ -373,7 +389,7 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (datagen recipe, generated on device)",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (datagen recipe, generated on device)",
             "qps": args.batch / (ms_step / 1e3),
             "latency_ms": lat_ms, "pipeline": pipe,
             "config": {"workload": workload_name(args, n_local), "n_items_per_gpu": n_local, "n_items_total": n_total,

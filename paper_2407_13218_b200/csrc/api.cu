@@ -138,13 +138,22 @@ constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) (static_assert in
 bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why) {
   const int dt = ix->d.dtype, dim = ix->d.dim;
   int nu = std::max(1, std::min(B, std::min(kMaxUsers, 8 / V)));
+  // The ring scan runs one user per launch: a user's key buffer then gets most of the shared
+  // memory the ring leaves (measured at c2 HIGH, B = 4 / 8: one launch per user 0.31 / 0.62 ms,
+  // users sharing a launch -- and its buffers, hence many compactions -- 0.81 / 2.48 ms).
+  const bool ws_ok = !std::getenv("LINR_NO_WS") && !std::getenv("LINR_MAX_NU");
+  const int nu_first = nu;
+  if (ws_ok) nu = 1;
+  if (const char* mn = std::getenv("LINR_MAX_NU")) nu = std::max(1, std::min(nu, std::atoi(mn)));
+  for (int pass = ws_ok ? 0 : 1; pass < 2; ++pass, nu = nu_first) {
   for (; nu >= 1; --nu) {
     const int nqv = next_pow2(nu * V);
     if (nqv > 8 || !scan_gemv_supported(dt, dim, nqv)) continue;
     const ScanCfg cfg = scan_gemv_cfg(dt, dim, nqv);
     if (cfg.nt == 0) continue;
     const int nw = cfg.nt / 32;
-    if (cfg.ws_slot_bytes > 0 && !std::getenv("LINR_NO_WS")) {
+    if (pass == 0 && cfg.ws_slot_bytes == 0) break;   // no ring kernel for this shape
+    if (pass == 0) {
       // ring scan (scan_ws.cuh): R (a power of two) slots of 16 rows, ~128 KB of rows in flight
       // by default; the rest of shared memory for the per-user key buffers (>= K + 256 keys)
       const int head = cfg.ws_cons_warps * 16;
@@ -179,6 +188,7 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
         pl->list_cap = (B <= 8) ? pl->bufcap : std::min(pl->bufcap, std::max(2 * K, 2048));
         return true;
       }
+      break;   // the ring kernel does not fit: per-warp kernel plans (pass 1)
     }
     const int head = nw * cfg.rows_per_iter;
     const size_t fixed = kScanCtlBytes + (size_t)nw * kTileItems * 2 + (size_t)nw * cfg.ring_bytes;
@@ -200,6 +210,7 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
     pl->grid = (pl->groups == 1 && ix->num_sms > 1) ? ix->num_sms - 1 : ix->num_sms;
     pl->list_cap = (B <= 8) ? pl->bufcap : std::min(pl->bufcap, std::max(2 * K, 2048));
     return true;
+  }
   }
   *why = "no GEMV scan configuration fits (dtype " + std::to_string(dt) + ", dim " + std::to_string(dim) +
          ", V " + std::to_string(V) + ", K " + std::to_string(K) + ")";

@@ -287,6 +287,7 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
   for (int u = 0; u < p.nu; ++u) {
     uint64_t* b = bufs + (size_t)u * p.bufcap;
     int n = min(ctl->count[u], p.bufcap);
+    bool sample_full64 = false;   // scratch64[32..64) holds candidates too (sorted with the rest)
     if (n > p.list_cap) {
       const uint64_t T = block_select_ge<NT>([b](int i) { return b[i]; }, n, p.K, &ctl->sel);
       n = block_compact_ge<NT>(b, n, T, &ctl->sel);
@@ -308,16 +309,35 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       }
       __syncthreads();
     } else if (n > kSample) {
-      // T0 = the 32nd largest of the threads' local maxima bounds the 32nd key from below (those
-      // 32 keys exist), so the top 32 are among the keys >= T0 -- usually a few dozen; collect
-      // them (cap kTailCand) and select among those. Fallback: select over the whole buffer.
+      // T0 = the 32nd largest of the threads' local maxima bounds the CTA's 32nd key from below
+      // (those 32 keys exist), so the top 32 are among the keys >= T0 -- usually a few dozen.
+      // T0 comes from a warp bitonic sort of each warp's 32 maxima and a tree of top-32 bitonic
+      // merges; the candidates >= T0 are sorted by one warp. Fallback: radix select.
       const int kTailCand = tail_cap;
       uint64_t* cand = scratch64 + 64;          // the rings are idle: room for kTailCand keys
       uint64_t mx = 0ull;
       for (int i = tid; i < n; i += NT) mx = b[i] > mx ? b[i] : mx;
-      cand[tid] = mx;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) mx = bitonic_pick(mx, shfl_xor_u64(mx, j), lane, k, j);
+      cand[tid] = mx;   // warp w's maxima, sorted descending, at cand[32w ..]
       __syncthreads();
-      const uint64_t T0 = block_select_ge<NT>([cand](int i) { return cand[i]; }, NT, kSample, &ctl->sel);
+      constexpr int NW = NT / 32;
+      for (int span = 1; span < NW; span <<= 1) {
+        if ((warp & (2 * span - 1)) == 0) {
+          const uint64_t x = cand[warp * 32 + lane], y = cand[(warp + span) * 32 + 31 - lane];
+          uint64_t v = x > y ? x : y;   // bitonic: the top 32 of the two lists
+#pragma unroll
+          for (int j = 16; j > 0; j >>= 1) {
+            const uint64_t pv = shfl_xor_u64(v, j);
+            v = ((lane & j) == 0) ? (v > pv ? v : pv) : (v < pv ? v : pv);
+          }
+          cand[warp * 32 + lane] = v;
+        }
+        __syncthreads();
+      }
+      const uint64_t T0 = cand[31];
       if (tid == 0) ctl->wcnt = 0;
       __syncthreads();
       for (int i0 = 0; i0 < n; i0 += NT) {
@@ -333,36 +353,46 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       }
       __syncthreads();
       const int m = ctl->wcnt;
-      const bool small = m <= kTailCand;
-      uint64_t T;
-      if (small) T = m > kSample ? block_select_ge<NT>([cand](int i) { return cand[i]; }, m, kSample, &ctl->sel) : 1ull;
-      else T = block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
-      if (tid == 0) ctl->wcnt = 0;
-      __syncthreads();
-      const int mm = small ? m : n;
-      const uint64_t* src = small ? cand : b;
-      for (int i0 = 0; i0 < mm; i0 += NT) {
-        const int i = i0 + tid;
-        const uint64_t v = i < mm ? src[i] : 0ull;
-        const bool top = i < mm && v >= T && v != 0ull;
-        const uint32_t bal = __ballot_sync(0xffffffffu, top);
-        int at = 0;
-        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
-        at = __shfl_sync(0xffffffffu, at, 0);
-        if (top) scratch64[at + __popc(bal & lanemask_lt())] = v;
+      if (m <= 64) {   // one warp sorts the candidates; the first 32 are the sample
+        sample_full64 = true;
+        if (warp == 0) {
+          scratch64[lane] = lane < m ? cand[lane] : 0ull;
+          scratch64[lane + 32] = lane + 32 < m ? cand[lane + 32] : 0ull;
+        }
+        __syncthreads();
+      } else {
+        const bool small = m <= kTailCand;
+        const uint64_t T = small ? block_select_ge<NT>([cand](int i) { return cand[i]; }, m, kSample, &ctl->sel)
+                                 : block_select_ge<NT>([b](int i) { return b[i]; }, n, kSample, &ctl->sel);
+        if (tid == 0) ctl->wcnt = 0;
+        __syncthreads();
+        const int mm = small ? m : n;
+        const uint64_t* src = small ? cand : b;
+        for (int i0 = 0; i0 < mm; i0 += NT) {
+          const int i = i0 + tid;
+          const uint64_t v = i < mm ? src[i] : 0ull;
+          const bool top = i < mm && v >= T && v != 0ull;
+          const uint32_t bal = __ballot_sync(0xffffffffu, top);
+          int at = 0;
+          if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
+          at = __shfl_sync(0xffffffffu, at, 0);
+          if (top) scratch64[at + __popc(bal & lanemask_lt())] = v;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     } else {
       for (int i = tid; i < kSample; i += NT) scratch64[i] = i < n ? b[i] : 0ull;
       __syncthreads();
     }
+    if (u == 0) dbg_mark(p.dbg, blockIdx.x * 8 + 2);
     uint64_t* samp = p.out_samp + ((size_t)u * gridDim.x + cta) * kSample;
     if (warp == 0) {
-      scratch64[32 + lane] = 0ull;
+      if (!sample_full64) scratch64[32 + lane] = 0ull;
       __syncwarp();
       warp_sort64_desc(scratch64);
       samp[lane] = scratch64[lane];
     }
+    if (u == 0) dbg_mark(p.dbg, blockIdx.x * 8 + 6);
     uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;
     for (int i = tid; i < n; i += NT) lst[i] = b[i];
     if (tid == 0) p.out_cnt[(size_t)u * gridDim.x + cta] = n;

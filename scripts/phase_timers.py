@@ -50,6 +50,8 @@ if (sc[:, 4] > 0).all():
     print(f"  first producer done  {q(rel(4))}")
     print(f"  last producer done   {q(rel(5))}")
 print(f"  scan loop end        {q(rel(1))}")
+print(f"  sample selected      {q(rel(2))}")
+print(f"  sample written       {q(rel(6))}")
 print(f"  tail end             {q(rel(3))}")
 print(f"  absolute tail end (from first start) max {((sc[:, 3] - t0) / 1e3).max():.2f} us")
 print(f"  compactions per CTA: min {sc[:,7].min()} med {np.median(sc[:,7])} max {sc[:,7].max()}")

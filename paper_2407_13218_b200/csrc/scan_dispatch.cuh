@@ -68,7 +68,7 @@ struct ScanDispatch {
     if constexpr (SG::kMma) {
       using W = WsGeom<DT, D>;
       static_assert(W::NT == nt<D, NQV>(), "both GEMV kernels run 512 threads");
-      return ScanCfg{nt<D, NQV>(), SG::RPI, SG::RING, W::SLOT, W::FIXED, W::NCW};
+      return ScanCfg{nt<D, NQV>(), SG::RPI, SG::RING, W::SLOT, W::FIXED, W::NCW * W::GR / 16};
     }
     return ScanCfg{nt<D, NQV>(), SG::RPI, SG::RING, 0, 0, 0};
   }

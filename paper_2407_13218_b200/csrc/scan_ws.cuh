@@ -32,7 +32,7 @@
 
 namespace linr {
 
-constexpr int kWsPcap = kTileItems + 16;   // pending-row list of a producer warp
+constexpr int kWsPcap = kTileItems + 32;   // pending-row list of a producer warp (tile + a group)
 
 LINR_DEV uint32_t ws_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 LINR_DEV void ws_bar_init(uint64_t* b, uint32_t count) {
@@ -83,7 +83,11 @@ struct WsGeom {
   static constexpr int NPW = 8;                  // producer warps (filter + gather)
   static constexpr int NCW = 8;                  // consumer warps (score + select)
   static constexpr int NT = 32 * (NPW + NCW);
-  static constexpr int SLOT = M::STAGE + 96;     // row group + 16 row ids + 16 user masks + 2 barriers
+  // rows per group: 32 for short rows (<= 128 B: the per-group scoring cost is amortised over
+  // as many bytes as a 16-row group of 256 B rows), 16 otherwise
+  static constexpr int GR = M::ROWB <= 128 ? 32 : 16;
+  static constexpr int GSTAGE = GR * M::ROWB;    // bytes of rows per group
+  static constexpr int SLOT = GSTAGE + GR * 5 + 16;   // rows + row ids + user masks + barrier + counter
   static constexpr int FIXED = 2048 + NPW * kWsPcap * 5 + 256;
 };
 
@@ -129,9 +133,9 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
   const int R = p.ring;                  // a power of two, multiple of NCW
   const int rshift = __ffs(R) - 1;
   uint32_t* mrow = reinterpret_cast<uint32_t*>(cur);
-  cur += (size_t)R * 64;
+  cur += (size_t)R * W::GR * 4;
   uint8_t* mmask = cur;
-  cur += (size_t)R * 16;
+  cur += (size_t)R * W::GR;
   uint64_t* fullb = reinterpret_cast<uint64_t*>(cur);
   int* rel = reinterpret_cast<int*>(fullb + R);   // times each slot was released by its consumer
   cur += (size_t)R * 16;
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
     };
     constexpr int LPRC = M::CH < 4 ? M::CH : 4;   // lanes per row in a copy step
     constexpr int RPS = 32 / LPRC;                 // rows per copy step
-    constexpr int NRS = M::ROWS / RPS;             // copy steps per group
+    constexpr int NRS = W::GR / RPS;               // copy steps per group
     constexpr int CPR = M::CH / LPRC;              // chunks per lane per row
     const int crow = lane / LPRC, cl = lane % LPRC;
     // one row group from pending entries [o, o+n), n <= 16 (rows past n are zero-filled, mask 0)
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       const int rnd = idx >> rshift, slot = idx & (R - 1);
       if (rnd > 0)
         while (ws_ld_acquire(&rel[slot]) < rnd) __nanosleep(32);
-      unsigned char* st = ring + (size_t)slot * M::STAGE;
+      unsigned char* st = ring + (size_t)slot * W::GSTAGE;
 #pragma unroll
       for (int rs = 0; rs < NRS; ++rs) {
         const int row = crow + rs * RPS;
@@ -206,9 +210,9 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
           cp_async16(dst + ((c ^ sw) * 16), src + c * 16, valid ? 16 : 0);
         }
       }
-      if (lane < 16) {
-        mrow[slot * 16 + lane] = lane < n ? prow[o + lane] : 0u;
-        mmask[slot * 16 + lane] = lane < n ? pm[o + lane] : (uint8_t)0;
+      if (lane < W::GR) {
+        mrow[slot * W::GR + lane] = lane < n ? prow[o + lane] : 0u;
+        mmask[slot * W::GR + lane] = lane < n ? pm[o + lane] : (uint8_t)0;
       }
       ws_cp_arrive(&fullb[slot]);
       __syncwarp();
@@ -303,9 +307,9 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       __syncwarp();
       // ---- full groups go to the ring; the remainder (< 16) moves to the front of the list
       int o = 0;
-      while (pc - o >= M::ROWS) {
-        emit(o, M::ROWS);
-        o += M::ROWS;
+      while (pc - o >= W::GR) {
+        emit(o, W::GR);
+        o += W::GR;
       }
       if (o > 0) {
         const int n = pc - o;
@@ -383,64 +387,74 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
         if (scan_flag(ctl, lane)) ws_compact<NCW * 32>(ctl, bufs, p, ctid);
       }
       if (!have) break;
-      const unsigned char* st = ring + (size_t)slot * M::STAGE;
+      const unsigned char* st = ring + (size_t)slot * W::GSTAGE;
       const uint32_t st_s = ws_su32(st);
-      // two independent accumulator chains (even / odd k-steps) halve the dependent mma latency
-      acc_t acc[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
+      constexpr int NSUB = W::GR / 16;   // m16 tiles per group
+      acc_t accs[NSUB][4];
 #pragma unroll
-      for (int ks = 0; ks < M::NKS; ++ks) {
-        uint32_t af[4];
-        const int chunk = ks * 2 + lhalf;
-        ldsm_x4(st_s + lrow * M::ROWB + ((chunk ^ M::swz(lrow)) * 16), af[0], af[1], af[2], af[3]);
-        acc_t (&c)[4] = (ks & 1) ? acc2 : acc;
-        if constexpr (kInt) mma32_s8(c, af, bq[ks][0], bq[ks][1]);
-        else mma16<DT>(c, af, bq[ks][0], bq[ks][1]);
+      for (int sb = 0; sb < NSUB; ++sb) {
+        // two independent accumulator chains (even / odd k-steps) halve the dependent mma latency
+        acc_t acc[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
+        const int row = sb * 16 + lrow;
+#pragma unroll
+        for (int ks = 0; ks < M::NKS; ++ks) {
+          uint32_t af[4];
+          const int chunk = ks * 2 + lhalf;
+          ldsm_x4(st_s + row * M::ROWB + ((chunk ^ M::swz(row)) * 16), af[0], af[1], af[2], af[3]);
+          acc_t (&c)[4] = (ks & 1) ? acc2 : acc;
+          if constexpr (kInt) mma32_s8(c, af, bq[ks][0], bq[ks][1]);
+          else mma16<DT>(c, af, bq[ks][0], bq[ks][1]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) accs[sb][i] = acc[i] + acc2[i];
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
-      // accumulator: acc[0..1] = row mg, columns 2mt, 2mt+1; acc[2..3] = row mg+8
+      // accumulator of tile sb: [0..1] = row sb*16 + mg, columns 2mt, 2mt+1; [2..3] = row + 8
       if constexpr (NQV == 1) {
-        // one user, one vector: column 0 lives in lanes mt == 0 (rows mg, mg+8); move row r's
-        // score to lane r so the 16 rows take one threshold test and one append
-        const uint32_t ent = lane < 16 ? (uint32_t)mmask[slot * 16 + lane] : 0u;
-        const uint32_t lr = lane < 16 ? mrow[slot * 16 + lane] : 0u;
+        // one user, one vector: column 0 lives in lanes mt == 0; move row r's score to lane r so
+        // the group's rows take one threshold test and one append
+        const uint32_t ent = lane < W::GR ? (uint32_t)mmask[slot * W::GR + lane] : 0u;
+        const uint32_t lr = lane < W::GR ? mrow[slot * W::GR + lane] : 0u;
         __syncwarp();
         if (lane == 0) ws_st_release(&rel[slot], rnd + 1);   // the slot's rows and metadata are consumed
         const int src = (lane & 7) * 4;
-        const acc_t x0 = __shfl_sync(0xffffffffu, acc[0], src);
-        const acc_t x2 = __shfl_sync(0xffffffffu, acc[2], src);
-        const float v = (float)((lane & 8) ? x2 : x0);
+        acc_t xv = 0;
+#pragma unroll
+        for (int sb = 0; sb < NSUB; ++sb) {
+          const acc_t x0 = __shfl_sync(0xffffffffu, accs[sb][0], src);
+          const acc_t x2 = __shfl_sync(0xffffffffu, accs[sb][2], src);
+          if ((lane >> 4) == sb) xv = (lane & 8) ? x2 : x0;
+        }
+        const float v = (float)xv;
         const bool cand = p.nu > 0 && (ent & 1u);
         Appender<NT, NU>::append(ctl, bufs, p, 0, cand, cand ? make_key(v, p.row0 + lr) : 0ull);
         if (scan_flag(ctl, lane)) ws_compact<NCW * 32>(ctl, bufs, p, ctid);
         continue;
       }
-      uint32_t ent[2], lr[2];
+      uint32_t ent[NSUB][2], lr[NSUB][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        ent[h] = mmask[slot * 16 + mg + 8 * h];
-        lr[h] = mrow[slot * 16 + mg + 8 * h];
-      }
+      for (int sb = 0; sb < NSUB; ++sb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          ent[sb][h] = mmask[slot * W::GR + sb * 16 + mg + 8 * h];
+          lr[sb][h] = mrow[slot * W::GR + sb * 16 + mg + 8 * h];
+        }
       __syncwarp();
       if (lane == 0) ws_st_release(&rel[slot], rnd + 1);   // the slot's rows and metadata are consumed
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t gid = p.row0 + lr[h];
-        const float v0 = (float)acc[2 * h], v1 = (float)acc[2 * h + 1];
-        if constexpr (NQV == 1) {
-          const bool cand = p.nu > 0 && mt == 0 && (ent[h] & 1u);
-          Appender<NT, NU>::append(ctl, bufs, p, 0, cand, cand ? make_key(v0, gid) : 0ull);
-        } else {
+      for (int sb = 0; sb < NSUB; ++sb)
 #pragma unroll
-          for (int u = 0; u < NU; ++u) {
-            float m = -INFINITY;
-            if (ucol0 == u) m = v0;
-            if (ucol1 == u) m = fmaxf(m, v1);
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-            const bool cand = u < p.nu && mt == 0 && ((ent[h] >> u) & 1u);
-            Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(m, gid) : 0ull);
-          }
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t gid = p.row0 + lr[sb][h];
+        const float v0 = (float)accs[sb][2 * h], v1 = (float)accs[sb][2 * h + 1];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          float m = -INFINITY;
+          if (ucol0 == u) m = v0;
+          if (ucol1 == u) m = fmaxf(m, v1);
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          const bool cand = u < p.nu && mt == 0 && ((ent[sb][h] >> u) & 1u);
+          Appender<NT, NU>::append(ctl, bufs, p, u, cand, cand ? make_key(m, gid) : 0ull);
         }
       }
       if (scan_flag(ctl, lane)) ws_compact<NCW * 32>(ctl, bufs, p, ctid);
@@ -463,7 +477,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
   for (int s = tid; s < R; s += NT) ws_bar_inval(&fullb[s]);   // the tail reuses this memory
   __syncthreads();
   dbg_mark(p.dbg, blockIdx.x * 8 + 1);
-  scan_tail<NT>(ctl, bufs, p, ring, smem_raw, (size_t)R * M::STAGE);
+  scan_tail<NT>(ctl, bufs, p, ring, smem_raw, (size_t)R * W::GSTAGE);
 }
 
 }  // namespace linr

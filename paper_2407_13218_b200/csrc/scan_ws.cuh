@@ -32,7 +32,7 @@
 
 namespace linr {
 
-constexpr int kWsPcap = kTileItems + 32;   // pending-row list of a producer warp (tile + a group)
+constexpr int kWsPcap = 2 * kTileItems + 32;   // pending-row list of a producer warp (<= 2 tiles + a group)
 
 LINR_DEV uint32_t ws_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 LINR_DEV void ws_bar_init(uint64_t* b, uint32_t count) {
@@ -244,6 +244,126 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       }
     };
     const bool only_w0 = p.wmask == 1u;
+    // clause evaluation of two tiles' word-0 attributes in one pass over the clause list (two
+    // independent dependency chains per clause: twice the ILP of one tile)
+    auto clauses_on2 = [&](const uint64_t (&a)[8], const uint64_t (&b)[8], uint32_t (&pa)[NU], uint32_t (&pbb)[NU]) {
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        if (u >= p.nu) continue;
+        for (int c = 0; c < p.ncl[u]; ++c) {
+          const KClause& k = p.cl[u][c];
+          const unsigned long long m = k.mask;
+          const uint32_t rev = k.rev ? 0xFFu : 0u;
+          uint32_t ha = 0, hb = 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            ha |= ((a[t] & m) != 0ull ? 1u : 0u) << t;
+            hb |= ((b[t] & m) != 0ull ? 1u : 0u) << t;
+          }
+          pa[u] &= ha ^ rev;
+          pbb[u] &= hb ^ rev;
+        }
+      }
+    };
+    auto live_bits = [&](uint32_t lw) -> uint32_t {   // bit t = item base + 32 t + lane
+      uint32_t mylive = 0xFFu;
+      if (!__all_sync(0xffffffffu, lw == ~0u)) {
+        mylive = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mylive |= ((__shfl_sync(0xffffffffu, lw, t) >> lane) & 1u) << t;
+      }
+      return mylive;
+    };
+    auto clauses_generic = [&](const uint64_t (&a)[8], int64_t base, uint32_t (&pb)[NU]) {
+#pragma unroll 1
+      for (int w = 0; w < 4; ++w) {
+        if (!((p.wmask >> w) & 1u)) continue;
+        uint64_t aw[8];
+        if (w == 0) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) aw[t] = a[t];
+        } else {
+          const uint64_t* ap = p.attr + (size_t)w * p.cap_pad + base + lane;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) aw[t] = ldg_stream_u64(ap + t * 32);
+        }
+        clauses_on(aw, (uint32_t)w, pb);
+      }
+    };
+    // Two tiles (A, B with tb > ta): clauses on their prefetched attribute words, refill the
+    // registers with the tiles four ahead (four register sets rotate through an unrolled loop:
+    // no register moves, which would wait for the loads), one pending-list append for both,
+    // full groups to the ring.
+    auto step2 = [&](int64_t& ta, uint64_t (&a)[8], uint32_t& la, int64_t& tb, uint64_t (&b)[8],
+                     uint32_t& lb) -> bool {
+      if (ta >= t_end) return false;
+      const bool hasb = tb < t_end;
+      const int64_t base_a = ta * kTileItems, base_b = tb * kTileItems;
+      const uint32_t live_a = live_bits(la), live_b = hasb ? live_bits(lb) : 0u;
+      uint32_t pa[NU], pbb[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        pa[u] = (u < p.nu) ? live_a : 0u;
+        pbb[u] = (u < p.nu) ? live_b : 0u;
+      }
+      if (only_w0) {
+        clauses_on2(a, b, pa, pbb);
+      } else {
+        clauses_generic(a, base_a, pa);
+        if (hasb) clauses_generic(b, base_b, pbb);
+      }
+      // the registers are free: refill them with the tiles four ahead
+      ta = grab();
+      if (ta < t_end) prefetch(ta, a, la);
+      tb = grab();
+      if (tb < t_end) prefetch(tb, b, lb);
+      // ---- append the passing rows of both tiles (order is irrelevant: keys carry ids)
+      uint32_t any = 0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        any |= pa[u] | (pbb[u] << 8);
+        pcnt[u] += __popc(pa[u]) + __popc(pbb[u]);
+      }
+      const int mine = __popc(any);
+      int incl = mine;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      int pos = pc + incl - mine;
+      while (any) {
+        const int t = __ffs(any) - 1;
+        any &= any - 1;
+        const bool inb = t >= 8;
+        const int tt = t & 7;
+        uint32_t um = 0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) um |= (((inb ? pbb[u] : pa[u]) >> tt) & 1u) << u;
+        prow[pos] = (uint32_t)((inb ? base_b : base_a) + tt * 32 + lane);
+        pm[pos] = (uint8_t)um;
+        ++pos;
+      }
+      pc += __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      // ---- full groups go to the ring; the remainder (< GR) moves to the front of the list
+      int o = 0;
+      while (pc - o >= W::GR) {
+        emit(o, W::GR);
+        o += W::GR;
+      }
+      if (o > 0) {
+        const int n = pc - o;
+        uint32_t r = 0;
+        uint8_t m = 0;
+        if (lane < n) { r = prow[o + lane]; m = pm[o + lane]; }
+        __syncwarp();
+        if (lane < n) { prow[lane] = r; pm[lane] = m; }
+        __syncwarp();
+        pc = n;
+      }
+      return true;
+    };
     auto step = [&](int64_t& tile, uint64_t (&a)[8], uint32_t& lw) -> bool {
       if (tile >= t_end) return false;
       const int64_t base = tile * kTileItems;
@@ -323,13 +443,26 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       }
       return true;
     };
-    int64_t t0 = grab(), t1 = grab(), t2 = grab();
-    uint64_t a0[8], a1[8], a2[8];
-    uint32_t l0 = 0, l1 = 0, l2 = 0;
-    if (t0 < t_end) prefetch(t0, a0, l0);
-    if (t1 < t_end) prefetch(t1, a1, l1);
-    if (t2 < t_end) prefetch(t2, a2, l2);
-    while (step(t0, a0, l0) && step(t1, a1, l1) && step(t2, a2, l2)) {
+    if constexpr (W::GR == 32) {
+      // short rows: the producers are the bottleneck (filter per item), two tiles per step
+      int64_t t0 = grab(), t1 = grab(), t2 = grab(), t3 = grab();
+      uint64_t a0[8], a1[8], a2[8], a3[8];
+      uint32_t l0 = ~0u, l1 = ~0u, l2 = ~0u, l3 = ~0u;
+      if (t0 < t_end) prefetch(t0, a0, l0);
+      if (t1 < t_end) prefetch(t1, a1, l1);
+      if (t2 < t_end) prefetch(t2, a2, l2);
+      if (t3 < t_end) prefetch(t3, a3, l3);
+      while (step2(t0, a0, l0, t1, a1, l1) && step2(t2, a2, l2, t3, a3, l3)) {
+      }
+    } else {
+      int64_t t0 = grab(), t1 = grab(), t2 = grab();
+      uint64_t a0[8], a1[8], a2[8];
+      uint32_t l0 = ~0u, l1 = ~0u, l2 = ~0u;
+      if (t0 < t_end) prefetch(t0, a0, l0);
+      if (t1 < t_end) prefetch(t1, a1, l1);
+      if (t2 < t_end) prefetch(t2, a2, l2);
+      while (step(t0, a0, l0) && step(t1, a1, l1) && step(t2, a2, l2)) {
+      }
     }
     if (pc > 0) emit(0, pc);
 #pragma unroll

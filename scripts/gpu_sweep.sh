@@ -6,4 +6,6 @@ run
 run --dtype i8 --dim 128 --items 12500000
 run --dtype i8 --dim 64 --items 125000000
 run --dtype bf16 --dim 64 --items 50000000
+run --preset LOW
+run --preset ALL
 run --dtype i8 --dim 128 --items 12500000 --preset ALL

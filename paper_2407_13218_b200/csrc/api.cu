@@ -494,7 +494,8 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   // LINR_FUSE_MERGE=1: the last CTAs of a single scan launch run the merge (saves a launch, but the
   // scan kernel then also carries the merge's latency); default: a separate merge kernel, which
   // overlaps the next search's scan when searches are pipelined on two streams
-  static const bool fuse_env = std::getenv("LINR_FUSE_MERGE") && std::atoi(std::getenv("LINR_FUSE_MERGE")) != 0;
+  const char* fe = std::getenv("LINR_FUSE_MERGE");
+  const bool fuse_env = fe && std::atoi(fe) != 0;
   const bool fused = pl.groups == 1 && fuse_env;
   for (int g = 0; g < pl.groups; ++g) {
     const int u0 = g * pl.nu_g;

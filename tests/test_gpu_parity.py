@@ -275,3 +275,17 @@ def test_batched_tensor_core_path(dtype, d, B, V, K, preset, n):
     assert prof["launches"] == 5, prof   # sample, threshold, main, finalize, pass count: the tcgen05 path ran
     ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what=f"tc dt{dtype} d{d} B{B} V{V}")
+
+
+# Kernel variants selected by the library's tuning knobs (read at plan time, per search): the
+# per-warp scan for tensor-core shapes (LINR_NO_WS), the merge fused into the scan's last CTAs
+# (LINR_FUSE_MERGE), a tiny per-user buffer (LINR_WS_CMAX: many consumer-side compactions while
+# the producers keep gathering) and a small ring (LINR_WS_RING_KB: slot reuse every few groups).
+@pytest.mark.parametrize("env", [{"LINR_NO_WS": "1"}, {"LINR_FUSE_MERGE": "1"}, {"LINR_WS_CMAX": "1280"},
+                                 {"LINR_WS_RING_KB": "16"}, {"LINR_WS_CMAX": "1280", "LINR_WS_RING_KB": "16"}])
+@pytest.mark.parametrize("dtype,d,B,V,preset", [(dg.BF16, 128, 1, 1, "ALL"), (dg.I8, 64, 1, 1, "HIGH"),
+                                                (dg.BF16, 64, 3, 2, "ALL"), (dg.I8, 128, 2, 1, "LOW")])
+def test_kernel_variants(monkeypatch, env, dtype, d, B, V, preset):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    run_case(dtype, d, 300_000, B, V, 1000, preset, dg.MODE_GRID, what=f"variant {env}")

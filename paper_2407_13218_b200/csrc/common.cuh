@@ -369,9 +369,11 @@ __device__ void block_sort_desc(uint64_t* s, int P2) {
 LINR_DEV void warp_sort64_desc(uint64_t* s) {
   const int lane = threadIdx.x & 31;
   uint64_t a = s[lane], b = s[lane + 32];
-#pragma unroll
+  // rolled loops: this runs once per CTA at the end of a scan, where the cold instruction fetch
+  // of an unrolled network costs more than the loop overhead
+#pragma unroll 1
   for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j == 32) {
         const uint64_t mx = a > b ? a : b, mn = a > b ? b : a;

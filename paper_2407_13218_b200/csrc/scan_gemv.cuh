@@ -317,9 +317,9 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       uint64_t* cand = scratch64 + 64;          // the rings are idle: room for kTailCand keys
       uint64_t mx = 0ull;
       for (int i = tid; i < n; i += NT) mx = b[i] > mx ? b[i] : mx;
-#pragma unroll
+#pragma unroll 1
       for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) mx = bitonic_pick(mx, shfl_xor_u64(mx, j), lane, k, j);
       cand[tid] = mx;   // warp w's maxima, sorted descending, at cand[32w ..]
       __syncthreads();
@@ -328,7 +328,7 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
         if ((warp & (2 * span - 1)) == 0) {
           const uint64_t x = cand[warp * 32 + lane], y = cand[(warp + span) * 32 + 31 - lane];
           uint64_t v = x > y ? x : y;   // bitonic: the top 32 of the two lists
-#pragma unroll
+#pragma unroll 1
           for (int j = 16; j > 0; j >>= 1) {
             const uint64_t pv = shfl_xor_u64(v, j);
             v = ((lane & j) == 0) ? (v > pv ? v : pv) : (v < pv ? v : pv);

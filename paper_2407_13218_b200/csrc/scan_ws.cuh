@@ -513,7 +513,8 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       }
       bool have = false;
       while (true) {
-        if (__all_sync(0xffffffffu, ws_bar_try(&fullb[slot], (uint32_t)rnd & 1u))) { have = true; break; }
+        if (__all_sync(0xffffffffu, ws_bar_test(&fullb[slot], (uint32_t)rnd & 1u))) { have = true; break; }
+        __nanosleep(20);
         int tot = 0;
         if (lane == 0) tot = *(volatile int*)&ctl->gtotal;
         if (idx >= __shfl_sync(0xffffffffu, tot, 0)) break;

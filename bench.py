@@ -308,14 +308,28 @@ def run_gpu(args):
 
     # ---------------- e2e through the host-buffer public API
     if sidx is None:
-        hids = torch.empty((args.batch, K), dtype=torch.int64, pin_memory=True)
-        hsc = torch.empty((args.batch, K), dtype=torch.float32, pin_memory=True)
-        hps = torch.empty(args.batch, dtype=torch.int64, pin_memory=True)
-        for _ in range(3):
-            ix.search_host(qpin, cls, K, out=(hids, hsc, hps))
+        # pipelined like the device-timed region: `pipe` streams, each with its own workspace and
+        # pinned result buffers; every step = query H2D + search + ids/scores/pass D2H, and a
+        # stream is synchronised (its results read back) before its buffers are reused
+        epipe = max(1, args.pipeline)
+        estreams = [torch.cuda.Stream(dev) for _ in range(epipe)]
+        ews = [ix.new_workspace(args.batch, 1, K, host_extra=True) for _ in range(epipe)]
+        eouts = [(torch.empty((args.batch, K), dtype=torch.int64, pin_memory=True),
+                  torch.empty((args.batch, K), dtype=torch.float32, pin_memory=True),
+                  torch.empty(args.batch, dtype=torch.int64, pin_memory=True)) for _ in range(epipe)]
+
+        def e2e_steps(n):
+            for k in range(n):
+                j = k % epipe
+                estreams[j].synchronize()
+                with torch.cuda.stream(estreams[j]):
+                    ix.search_host(qpin, cls, K, out=eouts[j], ws=ews[j], sync=False)
+            for s_ in estreams:
+                s_.synchronize()
+
+        e2e_steps(3 * epipe)
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            ix.search_host(qpin, cls, K, out=(hids, hsc, hps))
+        e2e_steps(args.steps)
         e2e_s = time.perf_counter() - t0
     else:
         for _ in range(3):

@@ -169,6 +169,17 @@ int linr_search_host(linr_index* index, const void* queries_host, int32_t B, int
                      void* ws_dev, size_t ws_bytes, int64_t* out_ids_host, float* out_scores_host,
                      int64_t* out_pass_host, void* stream);
 
+/* linr_search_host without the final synchronisation (pipelined serving: several searches in
+ * flight on different streams, each with its own ws_dev and host buffers). The query copy and the
+ * result copies are enqueued on `stream`; queries_host and the out_*_host buffers must be pinned
+ * and stay valid until `stream` has completed them (the caller synchronises the stream before it
+ * reads the results or reuses the buffers). Errors: as linr_search_host (copy errors may surface
+ * at the caller's synchronisation). */
+int linr_search_host_async(linr_index* index, const void* queries_host, int32_t B, int32_t V,
+                           const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
+                           void* ws_dev, size_t ws_bytes, int64_t* out_ids_host, float* out_scores_host,
+                           int64_t* out_pass_host, void* stream);
+
 /* Device-side synthetic data generator (benchmark plumbing, not part of the method): fills local
  * rows [row_begin, row_begin+n) of the index with the counter-based recipe of DESIGN.md
  * "Input recipe" (identical bytes to datagen/ in Python), marks them live and raises the

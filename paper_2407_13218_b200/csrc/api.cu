@@ -808,9 +808,27 @@ size_t linr_search_host_extra_bytes(const linr_index* ix, int32_t B, int32_t V, 
          align256((size_t)B * 8);
 }
 
+static int search_host_impl(linr_index* ix, const void* q_host, int32_t B, int32_t V, const linr_clause* cl,
+                            const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* ids_host,
+                            float* scores_host, int64_t* pass_host, void* stream, bool sync);
+
 int linr_search_host(linr_index* ix, const void* q_host, int32_t B, int32_t V, const linr_clause* cl,
                      const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* ids_host,
                      float* scores_host, int64_t* pass_host, void* stream) {
+  return search_host_impl(ix, q_host, B, V, cl, off, K, ws, ws_bytes, ids_host, scores_host, pass_host, stream,
+                          true);
+}
+
+int linr_search_host_async(linr_index* ix, const void* q_host, int32_t B, int32_t V, const linr_clause* cl,
+                           const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* ids_host,
+                           float* scores_host, int64_t* pass_host, void* stream) {
+  return search_host_impl(ix, q_host, B, V, cl, off, K, ws, ws_bytes, ids_host, scores_host, pass_host, stream,
+                          false);
+}
+
+static int search_host_impl(linr_index* ix, const void* q_host, int32_t B, int32_t V, const linr_clause* cl,
+                            const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* ids_host,
+                            float* scores_host, int64_t* pass_host, void* stream, bool sync) {
   if (!ix || !q_host || !ids_host || !scores_host) return fail(LINR_EINVAL, "null pointer");
   const size_t need = linr_search_workspace_bytes(ix, B, V, K);
   const size_t extra = linr_search_host_extra_bytes(ix, B, V, K);
@@ -834,7 +852,7 @@ int linr_search_host(linr_index* ix, const void* q_host, int32_t B, int32_t V, c
   e = cudaMemcpyAsync(ids_host, idd, (size_t)B * K * 8, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && pass_host) e = cudaMemcpyAsync(pass_host, psd, (size_t)B * 8, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && sync) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "search_host copies");
   return LINR_OK;
 }

@@ -22,7 +22,7 @@ ABI_FUNCTIONS = (
     "linr_storage_bytes", "linr_index_create", "linr_index_destroy", "linr_index_load",
     "linr_index_update_rows", "linr_index_delete_rows", "linr_index_stats",
     "linr_search_workspace_bytes", "linr_search", "linr_search_keys", "linr_merge_workspace_bytes",
-    "linr_merge_keys", "linr_search_host_extra_bytes", "linr_search_host", "linr_index_generate",
+    "linr_merge_keys", "linr_search_host_extra_bytes", "linr_search_host", "linr_search_host_async", "linr_index_generate",
     "linr_generate_rows", "linr_index_profile", "linr_index_profile_read", "linr_debug_timers", "linr_debug_read",
     "linr_last_error", "linr_version",
 )
@@ -70,6 +70,7 @@ def library():
         "linr_merge_keys": ([P, P, I32, I32, I32, P, SZ, P, P, P, P], ctypes.c_int),
         "linr_search_host_extra_bytes": ([P, I32, I32, I32], SZ),
         "linr_search_host": ([P, P, I32, I32, P, P, I32, P, SZ, P, P, P, P], ctypes.c_int),
+        "linr_search_host_async": ([P, P, I32, I32, P, P, I32, P, SZ, P, P, P, P], ctypes.c_int),
         "linr_index_generate": ([P, ctypes.c_uint64, I32, I64, I64, P], ctypes.c_int),
         "linr_generate_rows": ([I32, I32, I32, ctypes.c_uint64, I32, I64, I64, P, P, P], ctypes.c_int),
         "linr_index_profile": ([P, ctypes.c_int], ctypes.c_int),
@@ -220,11 +221,14 @@ class Index:
             self._ws[key] = ws
         return ws
 
-    def new_workspace(self, B: int, V: int, K: int) -> torch.Tensor:
+    def new_workspace(self, B: int, V: int, K: int, host_extra: bool = False) -> torch.Tensor:
         """A private search workspace (for searches overlapping on other streams)."""
-        n = library().linr_search_workspace_bytes(self._h, B, V, K)
+        L = library()
+        n = L.linr_search_workspace_bytes(self._h, B, V, K)
         if n == 0:
             raise LinrError(-1, f"no workspace for B={B} V={V} K={K}")
+        if host_extra:
+            n = ((n + 255) // 256) * 256 + L.linr_search_host_extra_bytes(self._h, B, V, K)
         return torch.empty(n, dtype=torch.uint8, device=self.device)
 
     def _q(self, queries: torch.Tensor):
@@ -271,9 +275,12 @@ class Index:
                                           ws.numel(), keys.data_ptr(), ps.data_ptr(), _stream(self.device)))
         return keys, ps
 
-    def search_host(self, queries_host: torch.Tensor, clauses, K: int, out=None):
+    def search_host(self, queries_host: torch.Tensor, clauses, K: int, out=None, ws=None, sync: bool = True):
         """End-to-end call with HOST buffers (pinned CPU tensors recommended): H2D of the queries,
-        search, D2H of ids/scores/pass, stream synchronised."""
+        search, D2H of ids/scores/pass, stream synchronised. sync=False (linr_search_host_async):
+        nothing is synchronised -- queries and outputs must be pinned and untouched until the
+        current stream completes; pass a private `ws` (new_workspace(..., host_extra=True)) per
+        stream when searches overlap."""
         q = queries_host if queries_host.dim() == 3 else queries_host[:, None, :]
         assert q.device.type == "cpu" and q.is_contiguous()
         B, V, _ = q.shape
@@ -284,8 +291,12 @@ class Index:
             ps = torch.empty(B, dtype=torch.int64, pin_memory=True)
         else:
             ids, sc, ps = out
-        ws = self.workspace(B, V, K, host_extra=True)
-        _check(library().linr_search_host(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
+        if ws is None:
+            ws = self.workspace(B, V, K, host_extra=True)
+        fn = library().linr_search_host if sync else library().linr_search_host_async
+        if not sync:
+            assert q.is_pinned() and ids.is_pinned() and sc.is_pinned() and ps.is_pinned(), "async host search needs pinned buffers"
+        _check(fn(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
                                           ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
                                           _stream(self.device)))
         return ids, sc, ps

@@ -212,6 +212,43 @@ def test_search_host_e2e_path():
     check(dg.BF16, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what="host")
 
 
+def test_search_host_async_pipelined():
+    """linr_search_host_async: searches of different queries in flight on two streams (own
+    workspaces, pinned host buffers), each equal to the oracle after its stream is synchronised."""
+    n, d, K = 200_000, 128, 1000
+    vals, attrs = dg.gen_items(3, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    cases = []
+    for j, preset in enumerate(["HIGH", "ALL", "LOW", "HIGH4"]):
+        Q = dg.gen_queries(10 + j, 3, n, 1, 1, d, dg.BF16, dg.MODE_GRID)
+        cls = dg.gen_clauses(10 + j, 1, preset)
+        qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16).contiguous().pin_memory()
+        out = (torch.empty((1, K), dtype=torch.int64, pin_memory=True),
+               torch.empty((1, K), dtype=torch.float32, pin_memory=True),
+               torch.empty(1, dtype=torch.int64, pin_memory=True))
+        cases.append((Q, cls, qh, out))
+    wss = [ix.new_workspace(1, 1, K, host_extra=True) for _ in streams]
+    for j, (Q, cls, qh, out) in enumerate(cases):
+        s = streams[j % 2]
+        s.synchronize()
+        if j >= 2:   # this stream's previous search has completed: check it before reuse
+            pQ, pcls, _, pout = cases[j - 2]
+            ref = oracle.search(dg.BF16, vals, attrs, np.ones(n), pQ, pcls, K)
+            check(dg.BF16, vals, attrs, np.ones(n), pQ, pcls, K, tuple(t.clone() for t in pout), ref, True, what="async")
+            cases[j - 2] = None
+        with torch.cuda.stream(s):
+            ix.search_host(qh, cls, K, out=out, ws=wss[j % 2], sync=False)
+    for s in streams:
+        s.synchronize()
+    for c in cases:
+        if c is None:
+            continue
+        Q, cls, _, out = c
+        ref = oracle.search(dg.BF16, vals, attrs, np.ones(n), Q, cls, K)
+        check(dg.BF16, vals, attrs, np.ones(n), Q, cls, K, out, ref, True, what="async")
+
+
 def test_concurrent_searches_on_streams():
     """Searches of one index in flight on several streams (own workspaces; the fused merge's
     per-search ticket slots) give the same results as the oracle, for many interleaved calls."""

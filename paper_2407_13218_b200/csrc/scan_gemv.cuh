@@ -340,16 +340,26 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       const uint64_t T0 = cand[31];
       if (tid == 0) ctl->wcnt = 0;
       __syncthreads();
-      for (int i0 = 0; i0 < n; i0 += NT) {
-        const int i = i0 + tid;
-        const uint64_t v = i < n ? b[i] : 0ull;
-        const bool top = i < n && v >= T0 && v != 0ull;
-        const uint32_t bal = __ballot_sync(0xffffffffu, top);
-        int at = 0;
-        if (lane == 0 && bal) at = atomicAdd(&ctl->wcnt, __popc(bal));
-        at = __shfl_sync(0xffffffffu, at, 0);
-        const int pos = at + __popc(bal & lanemask_lt());
-        if (top && pos < kTailCand) cand[pos] = v;
+      {   // collect the keys >= T0: count per thread, one warp scan and one atomic per warp
+        int c = 0;
+        for (int i = tid; i < n; i += NT) c += (b[i] >= T0) ? 1 : 0;   // keys are nonzero
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += t;
+        }
+        int base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&ctl->wcnt, incl);
+        int pos = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+        for (int i = tid; i < n && c > 0; i += NT) {
+          const uint64_t v = b[i];
+          if (v >= T0) {
+            if (pos < kTailCand) cand[pos] = v;
+            ++pos;
+            --c;
+          }
+        }
       }
       __syncthreads();
       const int m = ctl->wcnt;

@@ -399,8 +399,20 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
     if (warp == 0) {
       if (!sample_full64) scratch64[32 + lane] = 0ull;
       __syncwarp();
-      warp_sort64_desc(scratch64);
-      samp[lane] = scratch64[lane];
+      // rank sort of <= 64 distinct nonzero keys (zeros are padding): a key's position is the
+      // number of larger keys -- 32 independent broadcast steps instead of a 21-stage network
+      const uint64_t x0 = scratch64[lane], x1 = scratch64[lane + 32];
+      int r0 = 0, r1 = 0;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const uint64_t y0 = shfl_idx_u64(x0, j), y1 = shfl_idx_u64(x1, j);
+        r0 += (y0 > x0) + (y1 > x0);
+        r1 += (y0 > x1) + (y1 > x1);
+      }
+      samp[lane] = 0ull;
+      __syncwarp();
+      if (x0 != 0ull && r0 < kSample) samp[r0] = x0;
+      if (x1 != 0ull && r1 < kSample) samp[r1] = x1;
     }
     if (u == 0) dbg_mark(p.dbg, blockIdx.x * 8 + 6);
     uint64_t* lst = p.out_list + ((size_t)u * gridDim.x + cta) * p.list_cap;

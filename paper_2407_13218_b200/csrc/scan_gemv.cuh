@@ -317,11 +317,16 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
       uint64_t* cand = scratch64 + 64;          // the rings are idle: room for kTailCand keys
       uint64_t mx = 0ull;
       for (int i = tid; i < n; i += NT) mx = b[i] > mx ? b[i] : mx;
-#pragma unroll 1
-      for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) mx = bitonic_pick(mx, shfl_xor_u64(mx, j), lane, k, j);
-      cand[tid] = mx;   // warp w's maxima, sorted descending, at cand[32w ..]
+      {   // rank sort of the warp's 32 maxima: keys are distinct, only zero maxima (threads
+          // without keys) tie, and ties rank by lane
+        int r = 0;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+          const uint64_t y = shfl_idx_u64(mx, j);
+          r += (y > mx) || (y == mx && j < lane);
+        }
+        cand[warp * 32 + r] = mx;   // warp w's maxima, sorted descending, at cand[32w ..]
+      }
       __syncthreads();
       constexpr int NW = NT / 32;
       for (int span = 1; span < NW; span <<= 1) {

@@ -26,7 +26,8 @@ QUERY_SEED = 0x13218
 UPDATE_SEED = 0x4429
 
 # counter streams
-S_CLUSTER, S_CENTER, S_NOISE, S_ATTR, S_QROW, S_QNOISE, S_QCLAUSE = 1, 2, 3, 4, 5, 6, 7
+S_CLUSTER, S_CENTER, S_NOISE, S_ATTR, S_QROW, S_QNOISE, S_QCLAUSE, S_OPORP = 1, 2, 3, 4, 5, 6, 7, 8
+OPORP_SEED = 0x4294   # PAPER.md P:4294 (Sign-OPORP)
 
 N_CLUSTERS = 1024
 
@@ -310,3 +311,33 @@ def flatten_clauses(clauses):
         off.append(len(m))
     return (np.array(m, dtype=np.uint64), np.array(w, dtype=np.uint8),
             np.array(r, dtype=np.uint8), np.array(off, dtype=np.int32))
+
+
+# ---------------------------------------------------------------- Sign-OPORP parameters
+def oporp_params(seed: int, d: int, k: int):
+    """The random draws of Sign-OPORP (one permutation, one sign vector), as the
+    (src[L], sign[L]) arrays both the oracle and the library take (reading R25):
+      k <= d: the vector zero-padded to L = k*ceil(d/k), one uniform permutation of
+              the L positions: bins of ceil(d/k) entries (k = d: one coordinate per bit, the paper's
+              "1-bit embedding of the same dimension", P:4297);
+      k >  d: padding would leave k-d constant bits, so the vector is replicated k times (L = k*d)
+              and one uniform permutation of the L positions is taken: every bin sums d entries
+              (a sign random projection per bit).
+    src[p] = coordinate at position p (-1 = zero padding), sign[p] = +-1. Fisher-Yates over
+    SplitMix64 counters (seed, S_OPORP, p); signs from (seed, S_OPORP + 16, p)."""
+    if k % 64 or k < 64 or d < 1:
+        raise ValueError("k must be a positive multiple of 64")
+    if k <= d:
+        b = -(-d // k)
+        L = k * b
+        base = np.concatenate([np.arange(d, dtype=np.int64), np.full(L - d, -1, np.int64)])
+    else:
+        L = k * d
+        base = np.tile(np.arange(d, dtype=np.int64), k)
+    r = h1(seed, S_OPORP, np.arange(L, dtype=U64))
+    perm = base.copy()
+    for i in range(L - 1, 0, -1):   # Fisher-Yates: swap i with j = r[i] mod (i+1)
+        j = int(r[i] % U64(i + 1))
+        perm[i], perm[j] = perm[j], perm[i]
+    sgn = np.where((h1(seed, S_OPORP + 16, np.arange(L, dtype=U64)) & U64(1)) == U64(1), 1, -1).astype(np.int8)
+    return perm.astype(np.int32), sgn

@@ -4,6 +4,9 @@ Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl referen
 import this package. The product path (paper_2407_13218_b200) never imports it and shares no
 code with it. See linr_oracle.cpp for the definition and the PAPER.md passages it follows.
 
+oporp_oracle.cpp adds the quantised path (§3.2, Fig. 3): Sign-OPORP encoding, matched
+bits, the code search (any K, incl. huge K) and the V3 two-stage search.
+
 Parity status: every function is pinned in tests/test_oracle.py against values fixed by the
 paper's semantics and by mathematics (hand-worked example, closed forms, brute force,
 invariants). No function is "parity unpinned".
@@ -18,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "linr_oracle.cpp")
+_SRCS = [_SRC, os.path.join(_HERE, "oporp_oracle.cpp")]
 _LIB = os.path.join(_HERE, "liblinr_oracle.so")
 _lib = None
 
@@ -28,9 +32,9 @@ CLAUSE_DTYPE = np.dtype([("mask", "<u8"), ("word", "u1"), ("reverse", "u1"), ("p
 
 def build(force: bool = False) -> str:
     """Compile the oracle with plain g++ (no intrinsics, no BLAS)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", tmp, *_SRCS])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -54,6 +58,16 @@ def lib():
         L.oracle_merge.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P,
                                    ctypes.c_int, P, P, P]
         L.oracle_merge.restype = ctypes.c_int
+        I, I64 = ctypes.c_int, ctypes.c_int64
+        L.oracle_oporp_encode.argtypes = [I, I, I64, P, I, I, P, P, P]
+        L.oracle_oporp_encode.restype = I
+        L.oracle_matched_bits.argtypes = [I, I64, P, P, P]
+        L.oracle_matched_bits.restype = I
+        L.oracle_code_search.argtypes = [I, I, I64, I64, P, P, I, P, P, I, I, P, P, I64, I, I, P, P, P, P, P]
+        L.oracle_code_search.restype = I
+        L.oracle_search_v3.argtypes = [I, I, I64, I64, P, P, I, P, P, I, I, P, P, I, ctypes.c_double, I, I, P, P,
+                                       P, P, P, P]
+        L.oracle_search_v3.restype = I
         _lib = L
     return _lib
 
@@ -146,3 +160,78 @@ def merge(ids, scores_, pass_, K):
     if rc != 0:
         raise ValueError("oracle precondition violated")
     return oi, osc, op
+
+
+# ---------------------------------------------------------------- quantised path (oporp_oracle.cpp)
+def _prm(prm):
+    src, sign = prm
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    sign = np.ascontiguousarray(sign, dtype=np.int8)
+    return src, sign, len(src)
+
+
+def oporp_encode(dtype, emb, k, prm):
+    """Sign-OPORP codes [n][k/64] uint64 of rows emb [n][d] (storage repr). prm = (src, sign)."""
+    emb = np.ascontiguousarray(emb)
+    n, d = emb.shape
+    src, sign, L = _prm(prm)
+    out = np.zeros((n, k // 64), dtype=np.uint64)
+    if lib().oracle_oporp_encode(dtype, d, n, _p(emb), k, L, _p(src), _p(sign), _p(out)) != 0:
+        raise ValueError("oracle precondition violated")
+    return out
+
+
+def matched_bits(k, a, b):
+    a = np.ascontiguousarray(a, dtype=np.uint64).reshape(-1, k // 64)
+    b = np.ascontiguousarray(b, dtype=np.uint64).reshape(-1, k // 64)
+    out = np.zeros(len(a), dtype=np.int32)
+    if lib().oracle_matched_bits(k, len(a), _p(a), _p(b), _p(out)) != 0:
+        raise ValueError("oracle precondition violated")
+    return out
+
+
+def _search_inputs(emb, attrs, live, queries, clauses):
+    emb = np.ascontiguousarray(emb)
+    attrs = np.ascontiguousarray(attrs, dtype=np.uint64)
+    n, d = emb.shape
+    live = np.ascontiguousarray(live, dtype=np.uint8)
+    q = np.ascontiguousarray(queries)
+    if q.ndim == 2:
+        q = q[:, None, :]
+    ca, off = csr(clauses)
+    if len(ca) == 0:
+        ca = np.zeros(1, dtype=CLAUSE_DTYPE)
+    return emb, attrs, live, q, ca, off, n, d
+
+
+def code_search(dtype, emb, attrs, live, queries, clauses, K, k, prm, row0=0):
+    """Filtered top-K by matched bits (any K). Returns ids [B][K], m [B][K] int32 (-1 pad), pass [B]."""
+    emb, attrs, live, q, ca, off, n, d = _search_inputs(emb, attrs, live, queries, clauses)
+    B, V, _ = q.shape
+    src, sign, L = _prm(prm)
+    ids = np.zeros((B, K), dtype=np.int64)
+    m = np.zeros((B, K), dtype=np.int32)
+    ps = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_code_search(dtype, d, n, row0, _p(emb), _p(attrs), attrs.shape[1], _p(live), _p(q), B, V,
+                                  _p(ca), _p(off), K, k, L, _p(src), _p(sign), _p(ids), _p(m), _p(ps))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return ids, m, ps
+
+
+def search_v3(dtype, emb, attrs, live, queries, clauses, K, keep, k, prm, row0=0):
+    """V3: clause filter, keep K' by matched bits, full-precision rerank. Returns ids, scores (fp64),
+    pass, kept [B]."""
+    emb, attrs, live, q, ca, off, n, d = _search_inputs(emb, attrs, live, queries, clauses)
+    B, V, _ = q.shape
+    src, sign, L = _prm(prm)
+    ids = np.zeros((B, K), dtype=np.int64)
+    sc = np.zeros((B, K), dtype=np.float64)
+    ps = np.zeros(B, dtype=np.int64)
+    kept = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_search_v3(dtype, d, n, row0, _p(emb), _p(attrs), attrs.shape[1], _p(live), _p(q), B, V,
+                                _p(ca), _p(off), K, float(keep), k, L, _p(src), _p(sign), _p(ids), _p(sc), _p(ps),
+                                _p(kept))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return ids, sc, ps, kept

@@ -19,7 +19,8 @@
  *    memory (pinned or pageable). All data buffers are caller-owned (PyTorch allocates them);
  *    the library never frees them and they must outlive every call that uses them.
  *  - `stream` is a cudaStream_t passed as void*. All device work is enqueued on it; calls
- *    return before the work finishes, except linr_search_host and linr_index_stats, which
+ *    return before the work finishes, except linr_search_host, linr_index_stats and
+ *    linr_index_counters, which
  *    synchronise `stream`. A search observes exactly the updates enqueued before it on the same
  *    stream (snapshot consistency by stream order; reading R16). Searches (only searches) of one
  *    index may run concurrently on different streams, up to 16 in flight, each with its own
@@ -49,6 +50,7 @@ typedef enum {
   LINR_ERANGE = -2,       /* row range outside [global_row0, global_row0 + capacity)     */
   LINR_ENOMEM = -3,       /* workspace too small / host allocation failed                */
   LINR_ECUDA = -4,        /* CUDA launch / runtime error (sticky asynchronous errors too) */
+  LINR_ENCCL = -5,        /* NCCL failure (communicator creation / collective)           */
   LINR_EUNSUPPORTED = -6  /* valid but not built (e.g. a dim with no compiled kernel)     */
 } linr_status;
 
@@ -104,8 +106,9 @@ int linr_index_load(linr_index* index, int64_t row0, int64_t n, const void* emb_
 /* Live upsert (§4.3, "expose Upsert and Delete APIs"): overwrite rows
  * rows_dev[0..n) (global ids, device int64) in place with emb_dev [n][dim], attrs_dev [n][W];
  * mark them live; raise the high-water mark. Ids outside this shard are skipped on the device
- * and counted (linr_index_stats). If an id repeats within one call, which copy wins is
- * unspecified. A search on the same stream sees each row wholly old or wholly new. */
+ * and counted (linr_index_stats). If an id repeats within one call, its LAST occurrence wins
+ * (the earlier copies are not written). A search on the same stream sees each row wholly old or
+ * wholly new. Cost: one warp per entry, plus a scan of the later entries for duplicates. */
 int linr_index_update_rows(linr_index* index, const int64_t* rows_dev, int64_t n,
                            const void* emb_dev, const uint64_t* attrs_dev, void* stream);
 
@@ -118,6 +121,18 @@ int linr_index_delete_rows(linr_index* index, const int64_t* rows_dev, int64_t n
  * internal invariant that must stay 0; tests assert it). Any output may be NULL. */
 int linr_index_stats(linr_index* index, int64_t* hwm_host, int64_t* skipped_host,
                      int64_t* scan_overflow_host, void* stream);
+
+/* Synchronising read of all device-side counters (a superset of linr_index_stats):
+ *   hwm            high-water mark (local rows)
+ *   skipped        out-of-shard ids skipped by update/delete
+ *   scan_overflow  scan-buffer overflows (internal invariant, must stay 0)
+ *   tc_fallbacks   batched-path users whose pruned result could not be certified and were
+ *                  recomputed exactly on the device (reading R23; statistics only, results are
+ *                  exact either way) */
+typedef struct {
+  int64_t hwm, skipped, scan_overflow, tc_fallbacks;
+} linr_counters;
+int linr_index_counters(linr_index* index, linr_counters* out_host, void* stream);
 
 /* Workspace bytes needed by linr_search / linr_search_keys for (B, V, K). 0 if invalid. */
 size_t linr_search_workspace_bytes(const linr_index* index, int32_t B, int32_t V, int32_t K);
@@ -136,6 +151,22 @@ int linr_search(linr_index* index, const void* queries_dev, int32_t B, int32_t V
                 const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
                 void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, float* out_scores_dev,
                 int64_t* out_pass_dev, void* stream);
+
+/* Row sharding over GPUs (BASELINE.json north_star: "sharded row-wise across the 8 GPUs of one
+ * B200 box, each shard produces its local top-K, and an NCCL allgather of K (score, item-id)
+ * pairs over NVLink feeds a final merge"). One process per GPU, one index handle per shard
+ * (global_row0 = first global row of the shard).
+ *   linr_nccl_unique_id: out[128] = a fresh NCCL unique id (call on one rank, broadcast the bytes).
+ *   linr_comm_init: attach a communicator of `world` ranks (this handle is rank `rank`) to the
+ *     index; collective over the ranks (blocks until all have joined). Once attached, linr_search
+ *     and linr_search_host return the GLOBAL result on every rank: the shard's sorted keys and
+ *     pass counts are packed into one buffer of B*(K+1) u64, one ncclAllGather exchanges them and
+ *     the merge kernel reduces the world lists (exact, reading R13); out_pass is the global count.
+ *     linr_search_workspace_bytes includes the exchange buffers. The communicator is destroyed
+ *     with the index. NCCL is loaded at run time (libnccl.so.2); LINR_ENCCL if it is missing or
+ *     a collective fails. Ranks must call linr_search in the same order with the same B, V, K. */
+int linr_nccl_unique_id(uint8_t* out);
+int linr_comm_init(linr_index* index, const uint8_t* id, int32_t rank, int32_t world);
 
 /* Shard-local variant for row-sharded indexes: same inputs as linr_search, output is this
  * shard's top-K as packed keys out_keys_dev [B][K] u64 (sorted descending, 0-padded) plus
@@ -179,6 +210,67 @@ int linr_search_host_async(linr_index* index, const void* queries_host, int32_t 
                            const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
                            void* ws_dev, size_t ws_bytes, int64_t* out_ids_host, float* out_scores_host,
                            int64_t* out_pass_host, void* stream);
+
+/* ---------------------------------------------------------------- quantised KNN (§3.2)
+ * Sign-OPORP 1-bit codes ("Sign One Permutation One Random Projection ... compress
+ * embeddings to 1-bit and approximate dot-products via bitwise matching"). The projection is ONE
+ * permutation and ONE random sign vector of length L = bits * b, given as
+ *   src_host[L]  : the input coordinate at permuted position p, in [0, dim), or -1 (zero padding)
+ *   sign_host[L] : +1 / -1
+ * Bit j of a vector's code = [ sum_{p in [j*b, (j+1)*b)} sign[p] * x[src[p]] >= 0 ] (sum in fp64 in
+ * position order, so codes are deterministic; sign(0) = +); codes are bits/64 u64 words, LSB
+ * first. How src/sign are drawn (padding for bits <= dim, replication for bits > dim) is the
+ * caller's choice (reading R25; datagen.oporp_params). */
+typedef struct {
+  int32_t bits;              /* k: 64, 128, 256, 512 or 1024                          */
+  int32_t L;                 /* parameter length, a multiple of bits                  */
+  const int32_t* src_host;   /* [L]                                                   */
+  const int8_t* sign_host;   /* [L]                                                   */
+} linr_oporp_params;
+
+/* Bytes of the caller-owned device storage for the codes of every row + the parameters; 0 if the
+ * parameters are invalid. */
+size_t linr_codes_storage_bytes(const linr_index* index, const linr_oporp_params* params);
+
+/* Attach 1-bit codes to the index: copies the parameters, encodes every row below the high-water
+ * mark (setup call: synchronises `stream`, then enqueues the encoding on it). From then on load,
+ * update_rows and generate re-encode the rows they write, on the same stream (live updates keep
+ * the codes exact). EINVAL on bad parameters (src outside [-1, dim), sign not +-1, L % bits). */
+int linr_codes_attach(linr_index* index, const linr_oporp_params* params, void* code_storage_dev,
+                      void* stream);
+
+/* Encode n vectors x_dev [n][dim] (index dtype) with the attached parameters -> codes_dev
+ * [n][bits/64] u64 (the same arithmetic the index and the searches use). */
+int linr_oporp_encode(const linr_index* index, const void* x_dev, int64_t n, uint64_t* codes_dev,
+                      void* stream);
+
+/* Workspace for linr_code_search (v3 = 0) / linr_search_v3 (v3 = 1). 0 if invalid or no codes. */
+size_t linr_code_search_workspace_bytes(const linr_index* index, int32_t B, int32_t V, int64_t K,
+                                        int32_t v3);
+
+/* Filtered search ranked by matched bits only (Fig. 3 caption P:4310: "The quantized KNN module
+ * can be used without full precision matrix multiplication when K is large in top-K selection";
+ * top-50M of 1B). Per query: the clause filter (as linr_search), m(item) = max over the
+ * user's V query codes of popcount(NOT(q) XOR code(item)) = matched bits, results ordered by
+ * (m desc, id asc). K is UNBOUNDED (any K >= 1, up to the index size: exact selection by a
+ * counting sort over m in two passes). out_ids_dev [B][K] int64, out_matched_dev [B][K] int32;
+ * slots past min(K, pass) hold id -1 and m -1. out_pass_dev [B] may be NULL. */
+int linr_code_search(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
+                     const linr_clause* clauses_host, const int32_t* clause_off_host, int64_t K,
+                     void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, int32_t* out_matched_dev,
+                     int64_t* out_pass_dev, void* stream);
+
+/* V3 two-stage search ("leverage the approximated similarity as an extra pre-filtering
+ * step to reduce the computation of the full-precision matrix multiplication", Fig. 3; SPEC
+ * S:346-354): clause filter; keep the K' = min(pass, max(K, ceil(keep * pass))) best items by
+ * matched bits (m desc, id asc); re-score the kept items by the full-precision dot product (max
+ * over V, fp32 accumulation as linr_search) and return their top-K (score desc, id asc).
+ * keep in (0, 1]; keep = 1 is the exact search. K in [1, 2048]. out_kept_dev [B] (may be NULL) =
+ * K' per query. */
+int linr_search_v3(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
+                   const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
+                   double keep, void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev,
+                   float* out_scores_dev, int64_t* out_pass_dev, int64_t* out_kept_dev, void* stream);
 
 /* Device-side synthetic data generator (benchmark plumbing, not part of the method): fills local
  * rows [row_begin, row_begin+n) of the index with the counter-based recipe of DESIGN.md

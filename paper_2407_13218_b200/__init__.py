@@ -10,6 +10,6 @@ from __future__ import annotations
 
 from .linr import (  # noqa: F401
     F32, F16, BF16, I8, DTYPE_OF, LinrError, Index, merge_keys, library, lib_path,
-    clause_array, generate_rows,
+    clause_array, generate_rows, nccl_unique_id,
 )
 from .sharded import ShardedIndex, shard_range  # noqa: F401

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -26,6 +28,20 @@ ScanCfg scan_cfg_i8(int, int);
 static unsigned long long* g_dbg_host_ptr = nullptr;
 static bool g_dbg_on = false;
 unsigned long long* debug_buffer() { return g_dbg_on ? g_dbg_host_ptr : nullptr; }
+
+cudaError_t ensure_smem(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = granted[{kernel, dev}];
+  if (smem <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) have = smem;
+  return e;
+}
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
 
@@ -69,6 +85,8 @@ bool scan_gemv_supported(int dtype, int dim, int nqv) {
 
 using namespace linr;
 
+constexpr int kPinSlots = 16;
+
 struct ProfEvents {
   cudaEvent_t e0, e1, e2;   // before scan, after scan (= before merge), after merge
 };
@@ -78,13 +96,24 @@ struct linr_index {
   // batched tcgen05 path state
   CUtensorMap tmx;
   bool tmx_ok = false;
-  void* pin = nullptr;          // pinned staging for clauses / flags
-  size_t pin_bytes = 0;
-  cudaEvent_t pin_ev = nullptr;
+  // pinned staging ring for the batched path's clause tables: one slot per search in flight
+  // (ABI: up to 16), reused round-robin; a slot is reused once its previous copy has executed
+  struct PinSlot {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t ev = nullptr;
+  } pin[kPinSlots];
+  int pin_next = 0;
+  // Sign-OPORP 1-bit codes of the rows (linr_codes_attach): [cap_pad][code_k/64] u64 + params
+  uint64_t* codes = nullptr;
+  int code_k = 0, code_L = 0;
+  int32_t* c_src = nullptr;
+  int8_t* c_sign = nullptr;
+  void* comm = nullptr;         // NCCL communicator over the shards (linr_comm_init)
+  int comm_rank = 0, comm_world = 1;
   bool prof = false;
   std::vector<ProfEvents> prof_used, prof_free;
   int64_t prof_launches = 0;
-  int64_t tc_fallbacks = 0;     // batched-path users recomputed on the GEMV path
   uint64_t fuse_seq = 0;        // fused-merge ticket slot rotation
   bool force_gemv = false;
   int64_t cap_pad;
@@ -235,7 +264,7 @@ WsLayout ws_layout(const Plan& pl, int B, int K) {
 
 // ----------------------------------------------------------------- batched tcgen05 path
 struct TcWs {
-  size_t sbuf, scnt, thr, mbuf, mcnt, flags, cl, ncl, gemv, end;
+  size_t sbuf, scnt, thr, mbuf, mcnt, flags, cl, ncl, fb, bar, end;
 };
 int max_clauses(const int32_t* off, int B) {
   int m = 0;
@@ -252,8 +281,8 @@ bool use_tc(const linr_index* ix, int B, int V, int maxc, int wmax) {
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
 }
 bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
-  Plan g;
-  if (!make_plan(ix, 1, V, K, &g, why)) return false;   // exact GEMV fallback for uncertified users
+  (void)V;
+  (void)why;
   const size_t nu = (size_t)B;
   w->sbuf = 0;
   const size_t G = (size_t)ix->num_sms;
@@ -263,15 +292,52 @@ bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* 
   w->mcnt = align256(w->mbuf + nu * G * kTcMainCap * 8);
   w->flags = align256(w->mcnt + nu * G * 4);
   w->cl = align256(w->flags + nu * 4);
-  w->ncl = align256(w->cl + nu * 16 * sizeof(KClause));
-  w->gemv = align256(w->ncl + nu * 4);
-  w->end = w->gemv + ws_layout(g, 1, K).end;
+  w->ncl = w->cl + nu * 16 * sizeof(KClause);   // adjacent: one staging copy
+  w->fb = align256(w->ncl + nu * 4);
+  w->bar = align256(w->fb + fallback_ws_bytes(ix->num_sms, K));
+  w->end = w->bar + 256;
   return true;
 }
 
 int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
                 void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
                 int64_t* out_pass, cudaStream_t st);
+
+// Clause table [B][16] KClause followed by counts [B] int, copied host -> pinned slot -> dst_dev on
+// st (one copy). The pinned slot is reused kPinSlots calls later, once its copy has executed.
+int stage_clause_table(linr_index* ix, const linr_clause* cl, const int32_t* off, int B, void* dst_dev,
+                       cudaStream_t st) {
+  const size_t clb = (size_t)B * 16 * sizeof(KClause), nclb = (size_t)B * 4;
+  const size_t need = clb + nclb;
+  linr_index::PinSlot& ps = ix->pin[ix->pin_next];
+  ix->pin_next = (ix->pin_next + 1) % kPinSlots;
+  if (!ps.ev && cudaEventCreateWithFlags(&ps.ev, cudaEventDisableTiming) != cudaSuccess)
+    return fail(LINR_ECUDA, "staging event");
+  cudaEventSynchronize(ps.ev);   // the copy out of this slot (kPinSlots searches ago) has executed
+  if (ps.bytes < need) {
+    if (ps.p) cudaFreeHost(ps.p);
+    ps.p = nullptr;
+    ps.bytes = 0;
+    if (cudaHostAlloc(&ps.p, need, cudaHostAllocDefault) != cudaSuccess) return fail(LINR_ENOMEM, "pinned staging");
+    ps.bytes = need;
+  }
+  KClause* hcl = (KClause*)ps.p;
+  int* hncl = (int*)((char*)ps.p + clb);
+  std::memset(hcl, 0, clb);
+  for (int b = 0; b < B; ++b) {
+    hncl[b] = off[b + 1] - off[b];
+    for (int c = 0; c < hncl[b]; ++c) {
+      const linr_clause& k = cl[off[b] + c];
+      hcl[b * 16 + c].mask = k.mask;
+      hcl[b * 16 + c].word = k.word;
+      hcl[b * 16 + c].rev = k.reverse;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(dst_dev, ps.p, need, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(ps.ev, st);
+  if (e != cudaSuccess) return cuda_fail(e, "clause staging");
+  return LINR_OK;
+}
 
 int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
               void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
@@ -293,38 +359,11 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   std::memset(&p, 0, sizeof(p));
   p.tmx = ix->tmx;
   if (!tc_encode_map(&p.tmq, q, nvec, ix->rowbytes, np)) return fail(LINR_ECUDA, "cuTensorMapEncodeTiled failed for the queries");
-  // clauses: host -> pinned staging -> device (clause lists are host memory per the ABI)
-  const size_t clb = (size_t)B * 16 * sizeof(KClause), nclb = (size_t)B * 4, flb = (size_t)B * 4;
-  const size_t need = clb + nclb + flb;
-  if (!ix->pin_ev) cudaEventCreateWithFlags(&ix->pin_ev, cudaEventDisableTiming);
-  if (ix->pin_bytes < need) {
-    if (ix->pin) {
-      cudaEventSynchronize(ix->pin_ev);
-      cudaFreeHost(ix->pin);
-    }
-    ix->pin = nullptr;
-    if (cudaHostAlloc(&ix->pin, need, cudaHostAllocDefault) != cudaSuccess) return fail(LINR_ENOMEM, "pinned staging");
-    ix->pin_bytes = need;
-  } else {
-    cudaEventSynchronize(ix->pin_ev);   // the previous copy out of the staging buffer is done
+  // clauses: host -> pinned staging slot -> device (clause lists are host memory per the ABI)
+  {
+    const int rc = stage_clause_table(ix, cl, off, B, W + w.cl, st);   // cl and ncl are adjacent in ws
+    if (rc != LINR_OK) return rc;
   }
-  KClause* hcl = (KClause*)ix->pin;
-  int* hncl = (int*)((char*)ix->pin + clb);
-  int* hflags = (int*)((char*)ix->pin + clb + nclb);
-  std::memset(hcl, 0, clb);
-  for (int b = 0; b < B; ++b) {
-    hncl[b] = off[b + 1] - off[b];
-    for (int c = 0; c < hncl[b]; ++c) {
-      const linr_clause& k = cl[off[b] + c];
-      hcl[b * 16 + c].mask = k.mask;
-      hcl[b * 16 + c].word = k.word;
-      hcl[b * 16 + c].rev = k.reverse;
-    }
-  }
-  e = cudaMemcpyAsync(W + w.cl, hcl, clb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(W + w.ncl, hncl, nclb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaEventRecord(ix->pin_ev, st);
-  if (e != cudaSuccess) return cuda_fail(e, "batched staging");
 
   ProfEvents pe{};
   if (ix->prof) {
@@ -368,6 +407,8 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   p.thr = (const uint64_t*)(W + w.thr);
   p.buf = (uint64_t*)(W + w.mbuf);
   p.cap = kTcMainCap;
+  if (const char* mc = std::getenv("LINR_TC_MAIN_CAP"))   // test knob: small regions force the fallback
+    p.cap = std::max(1, std::min(kTcMainCap, std::atoi(mc)));
   p.cnt = (int*)(W + w.mcnt);
   p.sample_tiles = 0;
   p.dbg = debug_buffer();
@@ -375,10 +416,36 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   if (e != cudaSuccess) return cuda_fail(e, "tc main launch");
   if (ix->prof) cudaEventRecord(pe.e1, st);
   // 4. finalize
-  e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), kTcMainCap, ix->num_sms,
+  e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), p.cap, ix->num_sms,
                          (const uint64_t*)(W + w.thr), B, K, mode == 0 ? out_ids : nullptr,
-                         mode == 0 ? out_scores : nullptr, mode == 1 ? out_keys : nullptr, (int*)(W + w.flags), st);
+                         mode == 0 ? out_scores : nullptr, mode == 1 ? out_keys : nullptr, (int*)(W + w.flags),
+                         (unsigned int*)(W + w.bar), st);
   if (e != cudaSuccess) return cuda_fail(e, "tc finalize launch");
+  // 5. certification on the device: flagged users are recomputed exactly (fallback.cu); when no
+  //    user is flagged the launch reads the flags and exits. No host synchronisation.
+  FbParams fp;
+  std::memset(&fp, 0, sizeof(fp));
+  fp.emb = ix->emb;
+  fp.attr = ix->attr;
+  fp.cap_pad = ix->cap_pad;
+  fp.live = ix->live;
+  fp.hdr = ix->hdr;
+  fp.row0 = (uint32_t)ix->d.global_row0;
+  fp.dim = ix->d.dim;
+  fp.V = V;
+  fp.K = K;
+  fp.nu = B;
+  fp.q = q;
+  fp.cl = p.cl;
+  fp.ncl = p.ncl;
+  fp.flags = (const int*)(W + w.flags);
+  fp.lists = (uint64_t*)(W + w.fb);
+  fp.bar = (unsigned int*)(W + w.bar);
+  fp.out_ids = mode == 0 ? out_ids : nullptr;
+  fp.out_scores = mode == 0 ? out_scores : nullptr;
+  fp.out_keys = mode == 1 ? out_keys : nullptr;
+  e = launch_fallback(ix->d.dtype, fp, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tc fallback launch");
   if (out_pass) {
     e = cudaMemsetAsync(out_pass, 0, (size_t)B * 8, st);
     if (e == cudaSuccess)
@@ -389,21 +456,7 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   if (ix->prof) {
     cudaEventRecord(pe.e2, st);
     ix->prof_used.push_back(pe);
-    ix->prof_launches += 4 + (out_pass ? 1 : 0);
-  }
-  // 5. certify: users whose result is not provably exact are recomputed on the exact GEMV path
-  e = cudaMemcpyAsync(hflags, W + w.flags, flb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(e, "tc flags");
-  for (int b = 0; b < B; ++b) {
-    if (!hflags[b]) continue;
-    const int32_t off1[2] = {0, off[b + 1] - off[b]};
-    const int rc = search_impl(ix, (const char*)q + (size_t)b * V * ix->rowbytes, 1, V, cl + off[b], off1, K,
-                               W + w.gemv, ws_bytes - w.gemv, mode, out_ids ? out_ids + (size_t)b * K : nullptr,
-                               out_scores ? out_scores + (size_t)b * K : nullptr,
-                               out_keys ? out_keys + (size_t)b * K : nullptr, out_pass ? out_pass + b : nullptr, st);
-    if (rc != LINR_OK) return rc;
-    ix->tc_fallbacks++;
+    ix->prof_launches += 5 + (out_pass ? 1 : 0);
   }
   return LINR_OK;
 }
@@ -571,7 +624,7 @@ bool desc_ok(const linr_index_desc* d, std::string* why) {
 
 extern "C" {
 
-int linr_version(void) { return 1; }
+int linr_version(void) { return 2; }
 
 int linr_debug_timers(int enable) {
   unsigned long long* p = nullptr;
@@ -636,8 +689,14 @@ int linr_index_create(const linr_index_desc* d, linr_index** out) {
 
 void linr_index_destroy(linr_index* ix) {
   if (!ix) return;
-  if (ix->pin) cudaFreeHost(ix->pin);
-  if (ix->pin_ev) cudaEventDestroy(ix->pin_ev);
+  if (ix->comm) comm_destroy(ix->comm);
+  for (auto& ps : ix->pin) {
+    if (ps.ev) {
+      cudaEventSynchronize(ps.ev);
+      cudaEventDestroy(ps.ev);
+    }
+    if (ps.p) cudaFreeHost(ps.p);
+  }
   for (auto* v : {&ix->prof_used, &ix->prof_free})
     for (auto& pe : *v) {
       cudaEventDestroy(pe.e0);
@@ -693,6 +752,11 @@ int linr_index_load(linr_index* ix, int64_t row0, int64_t n, const void* emb, co
   if (e != cudaSuccess) return cuda_fail(e, "load attrs");
   e = launch_set_live_range(ix->live, ix->hdr, r0, n, st);
   if (e != cudaSuccess) return cuda_fail(e, "load live");
+  if (ix->codes) {   // keep the 1-bit codes in step with the rows (quantised embedding per item)
+    e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, n, r0, nullptr, 0, ix->d.capacity_rows, ix->code_k,
+                            ix->code_L, ix->c_src, ix->c_sign, ix->codes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "load encode");
+  }
   return LINR_OK;
 }
 
@@ -707,6 +771,11 @@ int linr_index_update_rows(linr_index* ix, const int64_t* rows, int64_t n, const
                                      ix->d.attr_words, ix->emb, ix->attr, ix->cap_pad, ix->live, ix->hdr,
                                      (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "update launch");
+  if (ix->codes) {   // re-encode the overwritten rows (after the update on the same stream)
+    e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, n, 0, rows, ix->d.global_row0, ix->d.capacity_rows,
+                            ix->code_k, ix->code_L, ix->c_src, ix->c_sign, ix->codes, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "update encode");
+  }
   return LINR_OK;
 }
 
@@ -736,7 +805,37 @@ int linr_index_stats(linr_index* ix, int64_t* hwm, int64_t* skipped, int64_t* ov
   return LINR_OK;
 }
 
+int linr_index_counters(linr_index* ix, linr_counters* out, void* stream) {
+  if (!ix || !out) return fail(LINR_EINVAL, "null argument");
+  DeviceGuard dg(ix->d.device);
+  DevHeader h;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(&h, ix->hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "counters");
+  out->hwm = (int64_t)h.hwm;
+  out->skipped = (int64_t)h.skipped;
+  out->scan_overflow = (int64_t)h.overflow;
+  out->tc_fallbacks = (int64_t)h.tc_fallbacks;
+  return LINR_OK;
+}
+
+static size_t local_ws_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K);
+
+// exchange buffers of a sharded search: send [B*(K+1)] u64, receive [world][B*(K+1)] u64
+static size_t comm_ws_bytes(const linr_index* ix, int32_t B, int32_t K) {
+  if (!ix->comm) return 0;
+  const size_t per = (size_t)B * (K + 1) * 8;
+  return align256(per) + align256(per * ix->comm_world);
+}
+
 size_t linr_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K) {
+  const size_t n = local_ws_bytes(ix, B, V, K);
+  if (n == 0) return 0;
+  return ix->comm ? align256(n) + comm_ws_bytes(ix, B, K) : n;
+}
+
+static size_t local_ws_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K) {
   if (!ix || B < 1 || V < 1 || V > 8 || K < 1 || K > LINR_MAX_K) return 0;
   Plan pl;
   std::string why;
@@ -749,11 +848,68 @@ size_t linr_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, i
   return n;
 }
 
+// With a communicator attached: shard-local keys + pass counts packed into one send buffer, one
+// ncclAllGather, one merge (every rank receives the global result). Without: the local search.
+static int search_global(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl,
+                         const int32_t* off, int32_t K, void* ws, size_t ws_bytes, int64_t* out_ids,
+                         float* out_scores, int64_t* out_pass, cudaStream_t st) {
+  if (!ix || !ix->comm)
+    return search_impl(ix, q, B, V, cl, off, K, ws, ws_bytes, 0, out_ids, out_scores, nullptr, out_pass, st);
+  if (!out_ids || !out_scores) return fail(LINR_EINVAL, "null outputs");
+  const size_t local = local_ws_bytes(ix, B, V, K);
+  if (local == 0) return fail(LINR_EINVAL, "bad B/V/K");
+  if (!ws || ws_bytes < align256(local) + comm_ws_bytes(ix, B, K)) return fail(LINR_ENOMEM, "workspace too small");
+  const size_t per = (size_t)B * (K + 1);
+  uint64_t* send = (uint64_t*)((char*)ws + align256(local));
+  uint64_t* recv = (uint64_t*)((char*)send + align256(per * 8));
+  int rc = search_impl(ix, q, B, V, cl, off, K, ws, local, 1, nullptr, nullptr, send, (int64_t*)(send + (size_t)B * K),
+                       st);
+  if (rc != LINR_OK) return rc;
+  DeviceGuard dg(ix->d.device);
+  rc = comm_allgather_u64(ix->comm, send, recv, per, st);
+  if (rc != LINR_OK) return rc;
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.samp = recv;            // each rank's list is sorted: its first min(K, 32) keys are its sample
+  mp.samp_sl = (int64_t)per;
+  mp.samp_su = K;
+  mp.ms = std::min(K, kScanSample);
+  mp.list = recv;
+  mp.list_sl = (int64_t)per;
+  mp.list_su = K;
+  mp.list_len = K;
+  mp.pass = (const int64_t*)(recv + (size_t)B * K);
+  mp.pstride_l = (int64_t)per;
+  mp.pstride_u = 1;
+  mp.L = ix->comm_world;
+  mp.K = K;
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_pass = out_pass;
+  mp.mode = 0;
+  mp.dbg = debug_buffer();
+  cudaError_t e = launch_merge(mp, B, st);
+  if (e != cudaSuccess) return cuda_fail(e, "shard merge launch");
+  return LINR_OK;
+}
+
 int linr_search(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,
                 int32_t K, void* ws, size_t ws_bytes, int64_t* out_ids, float* out_scores, int64_t* out_pass,
                 void* stream) {
-  return search_impl(ix, q, B, V, cl, off, K, ws, ws_bytes, 0, out_ids, out_scores, nullptr, out_pass,
-                     (cudaStream_t)stream);
+  return search_global(ix, q, B, V, cl, off, K, ws, ws_bytes, out_ids, out_scores, out_pass, (cudaStream_t)stream);
+}
+
+int linr_comm_init(linr_index* ix, const uint8_t* id, int32_t rank, int32_t world) {
+  if (!ix || !id) return fail(LINR_EINVAL, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LINR_EINVAL, "bad rank/world");
+  if (ix->comm) return fail(LINR_EINVAL, "a communicator is already attached");
+  void* c = nullptr;
+  const int rc = comm_create(ix->d.device, id, rank, world, &c);
+  if (rc != LINR_OK) return rc;
+  ix->comm = c;
+  ix->comm_rank = rank;
+  ix->comm_world = world;
+  return LINR_OK;
 }
 
 int linr_search_keys(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl,
@@ -847,7 +1003,7 @@ static int search_host_impl(linr_index* ix, const void* q_host, int32_t B, int32
   if (ws_bytes < align256(need) + extra) return fail(LINR_ENOMEM, "workspace too small");
   cudaError_t e = cudaMemcpyAsync(qd, q_host, (size_t)B * V * ix->rowbytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "query H2D");
-  int rc = search_impl(ix, qd, B, V, cl, off, K, ws, need, 0, idd, scd, nullptr, psd, st);
+  int rc = search_global(ix, qd, B, V, cl, off, K, ws, need, idd, scd, psd, st);
   if (rc != LINR_OK) return rc;
   e = cudaMemcpyAsync(ids_host, idd, (size_t)B * K * 8, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st);
@@ -871,6 +1027,11 @@ int linr_index_generate(linr_index* ix, uint64_t seed, int32_t mode, int64_t row
   if (e != cudaSuccess) return cuda_fail(e, "generate");
   e = launch_set_live_range(ix->live, ix->hdr, row_begin, n, st);
   if (e != cudaSuccess) return cuda_fail(e, "generate live");
+  if (ix->codes) {
+    e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, n, row_begin, nullptr, 0, ix->d.capacity_rows,
+                            ix->code_k, ix->code_L, ix->c_src, ix->c_sign, ix->codes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "generate encode");
+  }
   return LINR_OK;
 }
 
@@ -883,6 +1044,269 @@ int linr_generate_rows(int32_t dtype, int32_t dim, int32_t W, uint64_t seed, int
                                   (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "generate");
   return LINR_OK;
+}
+
+
+// ------------------------------------------------------------------ quantised path (codes.cu)
+static bool oporp_ok(const linr_index* ix, const linr_oporp_params* pr, std::string* why) {
+  if (!ix || !pr) { *why = "null argument"; return false; }
+  if (pr->bits < 64 || pr->bits > 1024 || pr->bits % 64 || ((pr->bits / 64) & (pr->bits / 64 - 1))) {
+    *why = "bits must be 64, 128, 256, 512 or 1024";
+    return false;
+  }
+  if (pr->L < pr->bits || pr->L % pr->bits || !pr->src_host || !pr->sign_host) { *why = "L must be a multiple of bits"; return false; }
+  for (int p = 0; p < pr->L; ++p) {
+    if (pr->src_host[p] < -1 || pr->src_host[p] >= ix->d.dim) { *why = "src entry outside [-1, dim)"; return false; }
+    if (pr->sign_host[p] != 1 && pr->sign_host[p] != -1) { *why = "sign entry not +-1"; return false; }
+  }
+  return true;
+}
+
+size_t linr_codes_storage_bytes(const linr_index* ix, const linr_oporp_params* pr) {
+  std::string why;
+  if (!oporp_ok(ix, pr, &why)) return 0;
+  return align256((size_t)ix->cap_pad * (pr->bits / 64) * 8) + align256((size_t)pr->L * 4) + align256((size_t)pr->L);
+}
+
+int linr_codes_attach(linr_index* ix, const linr_oporp_params* pr, void* storage, void* stream) {
+  std::string why;
+  if (!oporp_ok(ix, pr, &why)) return fail(LINR_EINVAL, why);
+  if (!storage) return fail(LINR_EINVAL, "null storage");
+  if (ix->codes) return fail(LINR_EINVAL, "codes already attached");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* b = (char*)storage;
+  uint64_t* codes = (uint64_t*)b;
+  int32_t* src = (int32_t*)(b + align256((size_t)ix->cap_pad * (pr->bits / 64) * 8));
+  int8_t* sign = (int8_t*)((char*)src + align256((size_t)pr->L * 4));
+  DevHeader h;
+  cudaError_t e = cudaStreamSynchronize(st);   // setup call: the rows to encode are those below the hwm now
+  if (e == cudaSuccess) e = cudaMemcpy(&h, ix->hdr, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(src, pr->src_host, (size_t)pr->L * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(sign, pr->sign_host, (size_t)pr->L, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "codes attach");
+  ix->codes = codes;
+  ix->code_k = pr->bits;
+  ix->code_L = pr->L;
+  ix->c_src = src;
+  ix->c_sign = sign;
+  e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, (int64_t)h.hwm, 0, nullptr, 0, ix->d.capacity_rows, ix->code_k,
+                          ix->code_L, src, sign, codes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "codes encode");
+  return LINR_OK;
+}
+
+int linr_oporp_encode(const linr_index* ix, const void* x, int64_t n, uint64_t* out, void* stream) {
+  if (!ix || !x || !out || n < 0) return fail(LINR_EINVAL, "bad argument");
+  if (!ix->codes) return fail(LINR_EINVAL, "no codes attached");
+  if (n == 0) return LINR_OK;
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = launch_oporp_encode(ix->d.dtype, x, ix->d.dim, n, 0, nullptr, 0, n, ix->code_k, ix->code_L, ix->c_src,
+                                      ix->c_sign, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "encode");
+  return LINR_OK;
+}
+
+namespace {
+constexpr int kCodeWarps = 16;   // warps per code-scan CTA (codes.cu kCodeNW)
+
+struct CodeWs {
+  size_t q, cl, kept, pass, mstar, T, H, off, marr, tmax, cand, lists, end;
+  int g;   // users per launch group
+};
+
+int code_group(const linr_index* ix, int B, int V) {
+  const int K1 = ix->code_k + 1;
+  int g = std::min(B, kCodeMaxUsers);
+  while (g > 1 && (code_hist_smem(g, V, ix->code_k) > ix->smem_optin ||
+                   (size_t)kCodeWarps * g * K1 * 4 > ix->smem_optin))
+    --g;
+  return g;
+}
+
+CodeWs code_layout(const linr_index* ix, int B, int V, int64_t K, bool v3) {
+  CodeWs w;
+  const int g = code_group(ix, B, V);
+  const size_t GW = (size_t)ix->num_sms * kCodeWarps, K1 = (size_t)ix->code_k + 1, words = ix->code_k / 64;
+  const size_t msz = ix->code_k <= 192 ? 1 : 2;
+  w.g = g;
+  w.q = 0;
+  w.cl = align256((size_t)B * V * words * 8);
+  w.kept = w.cl + align256((size_t)B * 16 * sizeof(KClause) + (size_t)B * 4);
+  w.pass = w.kept + align256((size_t)B * 8);
+  w.mstar = w.pass + align256((size_t)B * 8);
+  w.T = w.mstar + align256((size_t)g * 4);
+  w.H = w.T + align256((size_t)g * K1 * 8);
+  w.off = w.H + align256((size_t)g * GW * K1 * 4);
+  w.marr = w.off + align256((size_t)g * GW * K1 * 4);
+  w.tmax = w.marr + align256((size_t)g * ix->cap_pad * msz);
+  w.cand = w.tmax + align256((size_t)g * (ix->cap_pad / 256) * 2);
+  w.lists = w.cand + (v3 ? align256((size_t)g * ix->cap_pad * 4) : 0);
+  w.end = w.lists + (v3 ? align256((size_t)ix->num_sms * g * K * 8) : 0);
+  return w;
+}
+
+// the shared pipeline: query codes + clause table staged once; per user group: pass 1, offsets,
+// pass 2 (ids/m for the code search, kept rows for V3), and for V3 the rerank + merge.
+int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int64_t K,
+                  double keep, void* ws, size_t ws_bytes, int64_t* out_ids, int32_t* out_m, float* out_scores,
+                  int64_t* out_pass, int64_t* out_kept, cudaStream_t st) {
+  std::string why;
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (!ix->codes) return fail(LINR_EINVAL, "no codes attached (linr_codes_attach)");
+  int rc = validate_query(ix, q, B, V, cl, off, 1, &why);
+  if (rc != LINR_OK) return fail(rc, why);
+  const bool v3 = keep > 0.0;
+  if (K < 1 || (v3 && K > LINR_MAX_K)) return fail(LINR_EINVAL, v3 ? "K must be in [1, 2048]" : "K must be >= 1");
+  if (v3 && !(keep <= 1.0)) return fail(LINR_EINVAL, "keep must be in (0, 1]");
+  if (!out_ids || (!v3 && !out_m) || (v3 && !out_scores)) return fail(LINR_EINVAL, "null outputs");
+  const CodeWs w = code_layout(ix, B, V, K, v3);
+  if (!ws || ws_bytes < w.end) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+  char* W = (char*)ws;
+  const int words = ix->code_k / 64, K1 = ix->code_k + 1, GW = ix->num_sms * kCodeWarps;
+  const size_t msz = ix->code_k <= 192 ? 1 : 2;
+  uint64_t* qc = (uint64_t*)(W + w.q);
+  e = launch_oporp_encode(ix->d.dtype, q, ix->d.dim, (int64_t)B * V, 0, nullptr, 0, (int64_t)B * V, ix->code_k,
+                          ix->code_L, ix->c_src, ix->c_sign, qc, st);
+  if (e != cudaSuccess) return cuda_fail(e, "query encode");
+  rc = stage_clause_table(ix, cl, off, B, W + w.cl, st);
+  if (rc != LINR_OK) return rc;
+  const KClause* dcl = (const KClause*)(W + w.cl);
+  const int* dncl = (const int*)(W + w.cl + (size_t)B * 16 * sizeof(KClause));
+  int64_t* kept = (int64_t*)(W + w.kept);
+  int64_t* pass = out_pass ? out_pass : (int64_t*)(W + w.pass);
+  for (int u0 = 0; u0 < B; u0 += w.g) {
+    const int g = std::min(w.g, B - u0);
+    uint32_t wmask = 0;
+    for (int b = u0; b < u0 + g; ++b)
+      for (int c = off[b]; c < off[b + 1]; ++c) wmask |= 1u << cl[c].word;
+    e = cudaMemsetAsync(W + w.T, 0, (size_t)g * K1 * 8, st);
+    if (e != cudaSuccess) return cuda_fail(e, "code totals reset");
+    CodeScanParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.codes = ix->codes;
+    sp.attr = ix->attr;
+    sp.cap_pad = ix->cap_pad;
+    sp.live = ix->live;
+    sp.hdr = ix->hdr;
+    sp.nu = g;
+    sp.V = V;
+    sp.qcodes = qc + (size_t)u0 * V * words;
+    sp.cl = dcl + (size_t)u0 * 16;
+    sp.ncl = dncl + u0;
+    sp.wmask = wmask;
+    sp.marr = W + w.marr;
+    sp.tmax = (uint16_t*)(W + w.tmax);
+    sp.tmax_stride = ix->cap_pad / 256;
+    sp.H = (uint32_t*)(W + w.H);
+    sp.T = (unsigned long long*)(W + w.T);
+    e = launch_code_hist(ix->code_k, sp, ix->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "code pass 1 launch");
+    CodeOffsetParams op;
+    op.H = sp.H;
+    op.T = sp.T;
+    op.GW = GW;
+    op.k = ix->code_k;
+    op.K = K;
+    op.keep = keep;
+    op.off = (uint32_t*)(W + w.off);
+    op.mstar = (int*)(W + w.mstar);
+    op.kept = kept + u0;
+    op.pass = pass + u0;
+    e = launch_code_offsets(op, g, st);
+    if (e != cudaSuccess) return cuda_fail(e, "code offsets launch");
+    CodeEmitParams ep;
+    std::memset(&ep, 0, sizeof(ep));
+    ep.marr = W + w.marr;
+    ep.tmax = sp.tmax;
+    ep.tmax_stride = sp.tmax_stride;
+    ep.hdr = ix->hdr;
+    ep.cap_pad = ix->cap_pad;
+    ep.row0 = (uint32_t)ix->d.global_row0;
+    ep.nu = g;
+    ep.off = op.off;
+    ep.mstar = op.mstar;
+    ep.kept = op.kept;
+    if (v3) {
+      ep.out_stride = ix->cap_pad;
+      ep.cand = (uint32_t*)(W + w.cand);
+    } else {
+      ep.out_stride = K;
+      ep.out_ids = out_ids + (size_t)u0 * K;
+      ep.out_m = out_m + (size_t)u0 * K;
+    }
+    e = launch_code_emit(ix->code_k, ep, ix->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "code pass 2 launch");
+    if (!v3) {
+      e = launch_code_pad(op.kept, g, K, ep.out_ids, ep.out_m, ix->num_sms * 4, st);
+      if (e != cudaSuccess) return cuda_fail(e, "code pad launch");
+      continue;
+    }
+    RerankParams rp;
+    std::memset(&rp, 0, sizeof(rp));
+    rp.emb = ix->emb;
+    rp.row0 = (uint32_t)ix->d.global_row0;
+    rp.dim = ix->d.dim;
+    rp.V = V;
+    rp.K = (int)K;
+    rp.nu = g;
+    rp.q = (const char*)q + (size_t)u0 * V * ix->rowbytes;
+    rp.cand = ep.cand;
+    rp.cand_stride = ix->cap_pad;
+    rp.kept = op.kept;
+    rp.lists = (uint64_t*)(W + w.lists);
+    e = launch_rerank(ix->d.dtype, rp, ix->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rerank launch");
+    MergeParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.samp = rp.lists;                 // [cta][u][K], each list sorted: its first keys are its sample
+    mp.samp_sl = (int64_t)g * K;
+    mp.samp_su = K;
+    mp.ms = (int)std::min<int64_t>(K, kScanSample);
+    mp.list = rp.lists;
+    mp.list_sl = (int64_t)g * K;
+    mp.list_su = K;
+    mp.list_len = (int)K;
+    mp.L = ix->num_sms;
+    mp.K = (int)K;
+    mp.out_ids = out_ids + (size_t)u0 * K;
+    mp.out_scores = out_scores + (size_t)u0 * K;
+    mp.mode = 0;
+    mp.dbg = debug_buffer();
+    e = launch_merge(mp, g, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rerank merge launch");
+  }
+  if (out_kept) {
+    e = cudaMemcpyAsync(out_kept, kept, (size_t)B * 8, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "kept copy");
+  }
+  (void)msz;
+  return LINR_OK;
+}
+}  // namespace
+
+size_t linr_code_search_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, int64_t K, int32_t v3) {
+  if (!ix || !ix->codes || B < 1 || V < 1 || V > LINR_MAX_V || K < 1) return 0;
+  if (v3 && K > LINR_MAX_K) return 0;
+  return code_layout(ix, B, V, K, v3 != 0).end;
+}
+
+int linr_code_search(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,
+                     int64_t K, void* ws, size_t ws_bytes, int64_t* out_ids, int32_t* out_matched, int64_t* out_pass,
+                     void* stream) {
+  return code_pipeline(ix, q, B, V, cl, off, K, 0.0, ws, ws_bytes, out_ids, out_matched, nullptr, out_pass, nullptr,
+                       (cudaStream_t)stream);
+}
+
+int linr_search_v3(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,
+                   int32_t K, double keep, void* ws, size_t ws_bytes, int64_t* out_ids, float* out_scores,
+                   int64_t* out_pass, int64_t* out_kept, void* stream) {
+  if (!(keep > 0.0)) return fail(LINR_EINVAL, "keep must be in (0, 1]");
+  return code_pipeline(ix, q, B, V, cl, off, K, keep, ws, ws_bytes, out_ids, nullptr, out_scores, out_pass, out_kept,
+                       (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -29,7 +29,10 @@ __global__ void set_live_range_kernel(uint32_t* live, DevHeader* hdr, int64_t r0
   if (w == w0) atomicMax(&hdr->hwm, (unsigned long long)(r0 + n));
 }
 
-// one warp per updated row: copy the row (16-byte chunks), its attribute words, then publish it
+// one warp per updated row: copy the row (16-byte chunks), its attribute words, then publish it.
+// An id that repeats within one call is written once, by its LAST occurrence (last writer wins:
+// the warp of entry i skips if any later entry carries the same id), so a row is never a mix of
+// two copies.
 __global__ void update_rows_kernel(const int64_t* __restrict__ rows, int64_t n, int64_t grow0, int64_t cap,
                                    int rowbytes, const uint4* __restrict__ emb_src,
                                    const uint64_t* __restrict__ attr_src, int W, uint4* emb, uint64_t* attr,
@@ -37,10 +40,17 @@ __global__ void update_rows_kernel(const int64_t* __restrict__ rows, int64_t n, 
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
-  const int64_t r = rows[i] - grow0;
+  const int64_t gid = rows[i];
+  const int64_t r = gid - grow0;
   if (r < 0 || r >= cap) {
     if (lane == 0) atomicAdd(&hdr->skipped, 1ull);
     return;
+  }
+  bool later = false;
+  for (int64_t b = i + 1; b < n; b += 32) {   // warp-uniform trip count
+    const int64_t j = b + lane;
+    later = later || (j < n && rows[j] == gid);
+    if (__any_sync(0xffffffffu, later)) return;
   }
   const int ch = rowbytes / 16;
   for (int c = lane; c < ch; c += 32) emb[r * ch + c] = emb_src[i * ch + c];

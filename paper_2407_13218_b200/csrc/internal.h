@@ -19,6 +19,7 @@ struct DevHeader {               // lives in device memory
   // fused-merge tickets, one slot per in-flight search (searches may overlap across streams):
   unsigned int done_ctas[kFuseSlots];   // scan CTAs finished (self-resetting)
   unsigned int merged[kFuseSlots];      // users merged by the fused tail (self-resetting)
+  unsigned long long tc_fallbacks;      // batched-path users recomputed exactly (fallback.cu)
 };
 static_assert(sizeof(DevHeader) <= kHdrBytes, "device header too large");
 
@@ -144,7 +145,7 @@ cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap,
                                 int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st);
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
-                               cudaStream_t st);
+                               unsigned int* fb_bar, cudaStream_t st);
 cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
                             const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
                             cudaStream_t st);
@@ -152,6 +153,105 @@ constexpr int kTcSampleTiles = 8;
 constexpr int kTcSampleCap = 256;   // per (user, CTA) region of the sample: first passers in row order
 constexpr int kTcMainCap = 256;                      // per (user, CTA) region of the main pass
 
+
+// exact device-side recomputation of the batched path's uncertified users (fallback.cu)
+struct FbParams {
+  const void* emb;
+  const uint64_t* attr;
+  int64_t cap_pad;
+  const uint32_t* live;
+  DevHeader* hdr;
+  uint32_t row0;
+  int dim, V, K, nu;
+  const void* q;            // [nu][V][dim] index dtype
+  const KClause* cl;        // [nu][16]
+  const int* ncl;           // [nu]
+  const int* flags;         // [nu] 1 = recompute
+  uint64_t* lists;          // [2][grid][K] per-CTA top-K lists
+  unsigned int* bar;        // grid barrier counter, zeroed before the launch (tc_finalize_kernel)
+  int64_t* out_ids;         // [nu][K] (mode 0)
+  float* out_scores;
+  uint64_t* out_keys;       // [nu][K] (mode 1)
+};
+cudaError_t launch_fallback(int dtype, const FbParams& p, int grid, cudaStream_t st);
+size_t fallback_ws_bytes(int grid, int K);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
+// per device, so the cache is keyed by the current device ordinal.
+cudaError_t ensure_smem(const void* kernel, size_t smem);
+
+// ---------------------------------------------------------------- quantised path (codes.cu)
+constexpr int kCodeMaxUsers = 8;   // users per code-scan launch
+struct CodeScanParams {            // pass 1: filter + matched bits + histograms
+  const uint64_t* codes;           // [cap_pad][k/64]
+  const uint64_t* attr;
+  int64_t cap_pad;
+  const uint32_t* live;
+  const DevHeader* hdr;
+  int nu, V;
+  const uint64_t* qcodes;          // [nu][V][k/64] query codes (NOT applied in the kernel)
+  const KClause* cl;               // [nu][16]
+  const int* ncl;                  // [nu]
+  uint32_t wmask;                  // attribute words any clause reads
+  void* marr;                      // [nu][cap_pad] u8 (k <= 192) / u16 matched bits, none = 0xFF / 0xFFFF
+  uint16_t* tmax;                  // [nu][tmax_stride] per-tile max m (0xFFFF: no passing item)
+  int64_t tmax_stride;
+  uint32_t* H;                     // [nu][GW][k+1] per-warp histograms
+  unsigned long long* T;           // [nu][k+1] totals (zeroed before the launch)
+};
+struct CodeOffsetParams {
+  const uint32_t* H;
+  const unsigned long long* T;
+  int GW, k;
+  int64_t K;                       // results wanted (code search) / the K floor of V3
+  double keep;                     // > 0: V3 keep fraction
+  uint32_t* off;                   // [nu][GW][k+1] first output position (valid for m >= m*)
+  int* mstar;                      // [nu]
+  int64_t* kept;                   // [nu] positions to produce
+  int64_t* pass;                   // [nu] passing items (may be null)
+};
+struct CodeEmitParams {
+  const void* marr;
+  const uint16_t* tmax;
+  int64_t tmax_stride;
+  const DevHeader* hdr;
+  int64_t cap_pad;
+  uint32_t row0;
+  int nu;
+  const uint32_t* off;
+  const int* mstar;
+  const int64_t* kept;
+  int64_t out_stride;              // per-user stride of the outputs below
+  int64_t* out_ids;                // code search: ids, matched bits
+  int32_t* out_m;
+  uint32_t* cand;                  // V3: kept local rows
+};
+struct RerankParams {
+  const void* emb;
+  uint32_t row0;
+  int dim, V, K, nu;
+  const void* q;                   // [nu][V][dim]
+  const uint32_t* cand;            // [nu][cand_stride] local rows
+  int64_t cand_stride;
+  const int64_t* kept;             // [nu]
+  uint64_t* lists;                 // [grid][nu][K] sorted per-CTA top-K
+};
+cudaError_t launch_oporp_encode(int dtype, const void* x, int dim, int64_t n, int64_t row_begin, const int64_t* rows,
+                                int64_t grow0, int64_t cap, int k, int L, const int32_t* src, const int8_t* sign,
+                                uint64_t* codes, cudaStream_t st);
+size_t code_hist_smem(int nu, int V, int k);
+size_t rerank_smem(int V, int dim);
+cudaError_t launch_code_hist(int k, const CodeScanParams& p, int grid, cudaStream_t st);
+cudaError_t launch_code_offsets(const CodeOffsetParams& p, int nu, cudaStream_t st);
+cudaError_t launch_code_emit(int k, const CodeEmitParams& p, int grid, cudaStream_t st);
+cudaError_t launch_code_pad(const int64_t* kept, int nu, int64_t K, int64_t* out_ids, int32_t* out_m, int grid,
+                            cudaStream_t st);
+cudaError_t launch_rerank(int dtype, const RerankParams& p, int grid, cudaStream_t st);
+
+// NCCL communicator of a row-sharded index (comm.cu; NCCL loaded at run time)
+int comm_create(int device, const uint8_t id[128], int rank, int world, void** out);
+void comm_destroy(void* comm);
+int comm_allgather_u64(void* comm, const uint64_t* send, uint64_t* recv, size_t count, cudaStream_t st);
 
 void set_error(const std::string& msg);
 unsigned long long* debug_buffer();

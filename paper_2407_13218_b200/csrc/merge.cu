@@ -13,12 +13,8 @@ __global__ void __launch_bounds__(kMergeNT, 1) merge_kernel(const __grid_constan
 
 cudaError_t launch_merge(const MergeParams& p, int B, cudaStream_t st) {
   const size_t smem = merge_smem_bytes();
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(merge_kernel), smem);
+  if (e != cudaSuccess) return e;
   merge_kernel<<<B, kMergeNT, smem, st>>>(p);
   return cudaGetLastError();
 }

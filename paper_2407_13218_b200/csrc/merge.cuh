@@ -93,7 +93,8 @@ __device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
   __syncthreads();
   {   // pass counts: all loads in flight at once
     long long acc = 0;
-    for (int l = tid; l < L; l += NT) acc += p.pass[(int64_t)l * p.pstride_l + (int64_t)u * p.pstride_u];
+    if (p.pass)
+      for (int l = tid; l < L; l += NT) acc += p.pass[(int64_t)l * p.pstride_l + (int64_t)u * p.pstride_u];
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0 && acc) atomicAdd((unsigned long long*)&ctl->pass, (unsigned long long)acc);
   }

@@ -17,24 +17,16 @@ struct ScanDispatch {
     if constexpr (ScanGeom<DT, D, NQV>::kMma) {
       if (p.ring > 0) {   // warp-specialised kernel (the plan sized its ring)
         auto k = scan_ws_kernel<DT, D, NQV>;
-        static size_t smem_ws = 0;
-        if (smem > smem_ws) {
-          cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e != cudaSuccess) return e;
-          smem_ws = smem;
-        }
+        cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
+        if (e != cudaSuccess) return e;
         k<<<grid, WsGeom<DT, D>::NT, smem, st>>>(p);
         return cudaGetLastError();
       }
     }
     constexpr int NT = nt<D, NQV>();
     auto k = scan_gemv_kernel<DT, D, NQV, NT>;
-    static size_t smem_set = 0;   // opt-in size already granted to this instance
-    if (smem > smem_set) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      smem_set = smem;
-    }
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
+    if (e != cudaSuccess) return e;
     // grid = #SMs at one CTA per SM: every CTA is resident, so the fused merge's wait for the
     // other CTAs of the launch cannot deadlock (CTAs only wait on CTAs of the same launch).
     k<<<grid, NT, smem, st>>>(p);

@@ -65,6 +65,7 @@ struct RowGeom {
   static constexpr int RPW = 32 / LPR;          // rows per warp step
   static constexpr int R = CPL >= 4 ? 1 : 4 / CPL;  // rows in flight per lane group
   static constexpr int RPI = RPW * R;           // rows per warp iteration
+  static constexpr int STG = RPI * ROWB >= 4096 ? 2 : 4;   // cp.async ring depth (4 KB rows: 2, so 16 warps fit)
   static_assert(ROWB % 16 == 0, "row must be a multiple of 16 bytes");
   static_assert(CH % LPR == 0, "chunks must split evenly over the lanes of a row");
 };
@@ -149,7 +150,6 @@ struct ScanCtl {
 
 static_assert(sizeof(ScanCtl) + 16 <= 2048, "host plan reserves 2 KB for ScanCtl (api.cu kScanCtlBytes)");
 
-constexpr int kStages = 4;        // cp.async row-ring depth per warp
 constexpr int kSample = kScanSample;   // sorted per-CTA sample length (merge pruning)
 
 LINR_DEV bool scan_flag(const ScanCtl* ctl, int lane) {
@@ -272,7 +272,7 @@ struct ScanGeom {
   static constexpr bool kMma = MmaGeom<DT, D>::ok && NQV <= 8;
   static constexpr int RPI = kMma ? 16 : RowGeom<DT, D, NQV>::RPI;   // rows per warp iteration
   static constexpr int RING = kMma ? MmaGeom<DT, D>::S * MmaGeom<DT, D>::STAGE
-                                   : kStages * RowGeom<DT, D, NQV>::RPI * RowGeom<DT, D, NQV>::ROWB;
+                                   : RowGeom<DT, D, NQV>::STG * RowGeom<DT, D, NQV>::RPI * RowGeom<DT, D, NQV>::ROWB;
 };
 
 // Per-CTA output (sorted top-32 sample + every kept key) and the fused merge, run by all NT
@@ -702,7 +702,8 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
         if (scan_flag(ctl, lane)) scan_compact_all<NT>(ctl, bufs, p);
       }
     } else {
-      // ---- 2./3. CUDA-core path: LPR lanes per row, cp.async ring of kStages stages
+      // ---- 2./3. CUDA-core path: LPR lanes per row, cp.async ring of G::STG stages
+      constexpr int kStages = G::STG;
       const int n_iter = (cnt + G::RPI - 1) / G::RPI;
       constexpr int STAGE = G::RPI * G::ROWB;
       auto issue = [&](int it) {

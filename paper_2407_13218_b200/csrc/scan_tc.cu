@@ -17,7 +17,7 @@
 //      clauses only for the rare survivors (P:4266 semantics) and append survivors' keys.
 //   4. tc_finalize_kernel: per user, the K largest appended keys, sorted, decoded; a flag marks
 //      users whose result cannot be certified (buffer overflow, or T_u > 0 with fewer than K keys
-//      appended): the host re-runs those users through the exact GEMV path.
+//      appended); 5. fallback.cu recomputes the flagged users exactly on the device.
 // Exactness: every key >= T_u is appended; if at least K are, the K-th is >= T_u, so the top-K
 // of the buffer is the top-K of the user's passing items (reading R13-style argument).
 #include <cuda.h>
@@ -749,12 +749,14 @@ struct FinSmem {
 };
 __global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap, int grid,
                                                              const uint64_t* thr, int K, int64_t* out_ids,
-                                                             float* out_scores, uint64_t* out_keys, int* flags) {
+                                                             float* out_scores, uint64_t* out_keys, int* flags,
+                                                             unsigned int* fb_bar) {
   extern __shared__ __align__(16) unsigned char fsm[];
   FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
   uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
   uint64_t* s2 = s + kTcGatherCap;   // 4096 keys
   const int u = blockIdx.x, tid = threadIdx.x;
+  if (u == 0 && tid == 0) *fb_bar = 0u;   // the fallback kernel's grid barrier starts from zero
   long long total = 0;
   int n = gather_regions<512>(buf, cnt, grid, cap, u, s, kTcGatherCap, &f->n, &f->total, &total);
   const bool overflow = total > n;   // a region overflowed or the gather room was exceeded
@@ -855,12 +857,8 @@ template <int DT, int D, int NP>
 static cudaError_t launch_tc_np(const TcParams& p, int grid, cudaStream_t st) {
   const size_t smem = tc_lay(NP, TcGeom<DT, D>::ROWB, p.nu, p.maxc, p.wmax).bytes;
   auto k = tc_scan_kernel<DT, D, NP>;
-  static size_t set = 0;
-  if (smem > set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
+  if (e != cudaSuccess) return e;
   k<<<grid, kTcThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -908,27 +906,20 @@ cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int gr
 cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
                                 int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st) {
   const size_t smem = ((sizeof(SelScratch) + 32 + 15) & ~size_t(15)) + (size_t)kTcGatherCap * 8;
-  static size_t set = 0;
-  if (smem > set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_threshold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_threshold_kernel), smem);
+  if (e != cudaSuccess) return e;
   tc_threshold_kernel<<<nu, 512, smem, st>>>(sbuf, scnt, scap, grid, nu, K, sample_items, hdr, thr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
-                               cudaStream_t st) {
+                               unsigned int* fb_bar, cudaStream_t st) {
   const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcGatherCap + 4096) * 8;
-  static size_t set = 0;
-  if (smem > set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
-  tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags);
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_finalize_kernel), smem);
+  if (e != cudaSuccess) return e;
+  tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags,
+                                            fb_bar);
   return cudaGetLastError();
 }
 

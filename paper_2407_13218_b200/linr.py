@@ -24,7 +24,9 @@ ABI_FUNCTIONS = (
     "linr_search_workspace_bytes", "linr_search", "linr_search_keys", "linr_merge_workspace_bytes",
     "linr_merge_keys", "linr_search_host_extra_bytes", "linr_search_host", "linr_search_host_async", "linr_index_generate",
     "linr_generate_rows", "linr_index_profile", "linr_index_profile_read", "linr_debug_timers", "linr_debug_read",
-    "linr_last_error", "linr_version",
+    "linr_last_error", "linr_version", "linr_index_counters", "linr_nccl_unique_id", "linr_comm_init",
+    "linr_codes_storage_bytes", "linr_codes_attach", "linr_oporp_encode", "linr_code_search_workspace_bytes",
+    "linr_code_search", "linr_search_v3",
 )
 
 
@@ -32,6 +34,16 @@ class LinrError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"linr error {code}: {msg}")
         self.code = code
+
+
+class _Counters(ctypes.Structure):
+    _fields_ = [("hwm", ctypes.c_int64), ("skipped", ctypes.c_int64), ("scan_overflow", ctypes.c_int64),
+                ("tc_fallbacks", ctypes.c_int64)]
+
+
+class _Oporp(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_int32), ("L", ctypes.c_int32), ("src_host", ctypes.c_void_p),
+                ("sign_host", ctypes.c_void_p)]
 
 
 class _Desc(ctypes.Structure):
@@ -63,6 +75,15 @@ def library():
         "linr_index_update_rows": ([P, P, I64, P, P, P], ctypes.c_int),
         "linr_index_delete_rows": ([P, P, I64, P], ctypes.c_int),
         "linr_index_stats": ([P, PI64, PI64, PI64, P], ctypes.c_int),
+        "linr_index_counters": ([P, ctypes.POINTER(_Counters), P], ctypes.c_int),
+        "linr_nccl_unique_id": ([P], ctypes.c_int),
+        "linr_codes_storage_bytes": ([P, ctypes.POINTER(_Oporp)], SZ),
+        "linr_codes_attach": ([P, ctypes.POINTER(_Oporp), P, P], ctypes.c_int),
+        "linr_oporp_encode": ([P, P, I64, P, P], ctypes.c_int),
+        "linr_code_search_workspace_bytes": ([P, I32, I32, I64, I32], SZ),
+        "linr_code_search": ([P, P, I32, I32, P, P, I64, P, SZ, P, P, P, P], ctypes.c_int),
+        "linr_search_v3": ([P, P, I32, I32, P, P, I32, ctypes.c_double, P, SZ, P, P, P, P, P], ctypes.c_int),
+        "linr_comm_init": ([P, P, I32, I32], ctypes.c_int),
         "linr_search_workspace_bytes": ([P, I32, I32, I32], SZ),
         "linr_search": ([P, P, I32, I32, P, P, I32, P, SZ, P, P, P, P], ctypes.c_int),
         "linr_search_keys": ([P, P, I32, I32, P, P, I32, P, SZ, P, P, P], ctypes.c_int),
@@ -164,6 +185,88 @@ class Index:
     def handle(self):
         return self._h
 
+    def attach_comm(self, unique_id: bytes, rank: int, world: int):
+        """Attach an NCCL communicator over the shards (linr_comm_init; collective). Afterwards
+        search()/search_host() return the global result on every rank."""
+        assert len(unique_id) == 128
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        torch.cuda.synchronize(self.device)
+        _check(library().linr_comm_init(self._h, ctypes.addressof(buf), rank, world))
+        self._ws = {}   # workspaces grow by the exchange buffers
+        self.comm_world = world
+
+    # ------------------------------------------------------------ quantised path (PAPER.md §3.2)
+    def attach_codes(self, bits: int, src, sign):
+        """Attach Sign-OPORP codes (linr_codes_attach): src int32[L] / sign int8[L] host arrays
+        (e.g. datagen.oporp_params). Encodes the current rows; later loads/updates re-encode."""
+        src = np.ascontiguousarray(src, dtype=np.int32)
+        sign = np.ascontiguousarray(sign, dtype=np.int8)
+        prm = _Oporp(bits, len(src), src.ctypes.data, sign.ctypes.data)
+        L = library()
+        n = L.linr_codes_storage_bytes(self._h, ctypes.byref(prm))
+        if n == 0:
+            raise LinrError(-1, "invalid Sign-OPORP parameters")
+        self.code_storage = torch.empty(n, dtype=torch.uint8, device=self.device)
+        _check(L.linr_codes_attach(self._h, ctypes.byref(prm), self.code_storage.data_ptr(), _stream(self.device)))
+        self.code_bits = bits
+        self._cws = {}
+
+    def codes(self, n: int | None = None) -> torch.Tensor:
+        """View of the stored codes [n][bits/64] (int64 view of the u64 words)."""
+        n = self.capacity if n is None else n
+        return self.code_storage[:n * self.code_bits // 8].view(torch.int64).view(n, self.code_bits // 64)
+
+    def encode(self, x: torch.Tensor) -> torch.Tensor:
+        """linr_oporp_encode of vectors x [n][dim] (index dtype, device) -> [n][bits/64] int64."""
+        x = x.contiguous()
+        assert x.dtype == TORCH_DTYPE[self.dtype] and x.shape[-1] == self.dim and x.device == self.device
+        out = torch.empty((x.shape[0], self.code_bits // 64), dtype=torch.int64, device=self.device)
+        _check(library().linr_oporp_encode(self._h, x.data_ptr(), x.shape[0], out.data_ptr(), _stream(self.device)))
+        return out
+
+    def _code_ws(self, B, V, K, v3):
+        key = (B, V, K, v3)
+        ws = self._cws.get(key)
+        if ws is None:
+            n = library().linr_code_search_workspace_bytes(self._h, B, V, K, 1 if v3 else 0)
+            if n == 0:
+                raise LinrError(-1, f"no code-search workspace for B={B} V={V} K={K}")
+            ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+            self._cws[key] = ws
+        return ws
+
+    def code_search(self, queries: torch.Tensor, clauses, K: int):
+        """Filtered top-K by matched bits, any K (linr_code_search). Returns ids [B][K] int64,
+        matched [B][K] int32, pass [B] int64 on the device."""
+        q = self._q(queries)
+        B, V, _ = q.shape
+        cl = clause_array(clauses)
+        assert cl.B == B, "one clause list per query"
+        ids = torch.empty((B, K), dtype=torch.int64, device=self.device)
+        m = torch.empty((B, K), dtype=torch.int32, device=self.device)
+        ps = torch.empty(B, dtype=torch.int64, device=self.device)
+        ws = self._code_ws(B, V, K, False)
+        _check(library().linr_code_search(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
+                                          ws.numel(), ids.data_ptr(), m.data_ptr(), ps.data_ptr(),
+                                          _stream(self.device)))
+        return ids, m, ps
+
+    def search_v3(self, queries: torch.Tensor, clauses, K: int, keep: float):
+        """V3 two-stage search (linr_search_v3). Returns ids, scores, pass, kept on the device."""
+        q = self._q(queries)
+        B, V, _ = q.shape
+        cl = clause_array(clauses)
+        assert cl.B == B, "one clause list per query"
+        ids = torch.empty((B, K), dtype=torch.int64, device=self.device)
+        sc = torch.empty((B, K), dtype=torch.float32, device=self.device)
+        ps = torch.empty(B, dtype=torch.int64, device=self.device)
+        kept = torch.empty(B, dtype=torch.int64, device=self.device)
+        ws = self._code_ws(B, V, K, True)
+        _check(library().linr_search_v3(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, float(keep),
+                                        ws.data_ptr(), ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
+                                        kept.data_ptr(), _stream(self.device)))
+        return ids, sc, ps, kept
+
     # ------------------------------------------------------------ maintenance
     def load(self, emb: torch.Tensor, attrs: torch.Tensor, row0: int | None = None):
         row0 = self.row0 if row0 is None else row0
@@ -178,12 +281,17 @@ class Index:
         rows = rows.to(torch.int64).contiguous()
         emb = emb.contiguous()
         attrs = _as_i64(attrs).contiguous()
+        n = rows.numel()
+        assert rows.device == self.device and emb.device == self.device and attrs.device == self.device, \
+            "update buffers must live on the index's device"
         assert emb.dtype == TORCH_DTYPE[self.dtype]
+        assert tuple(emb.shape) == (n, self.dim) and tuple(attrs.shape) == (n, self.W), "update shapes"
         _check(library().linr_index_update_rows(self._h, rows.data_ptr(), rows.numel(), emb.data_ptr(),
                                                 attrs.data_ptr(), _stream(self.device)))
 
     def delete_rows(self, rows: torch.Tensor):
         rows = rows.to(torch.int64).contiguous()
+        assert rows.device == self.device, "delete ids must live on the index's device"
         _check(library().linr_index_delete_rows(self._h, rows.data_ptr(), rows.numel(), _stream(self.device)))
 
     def generate(self, seed: int, mode: int, row_begin: int, n: int):
@@ -195,6 +303,13 @@ class Index:
         _check(library().linr_index_stats(self._h, ctypes.byref(hwm), ctypes.byref(sk), ctypes.byref(ov),
                                           _stream(self.device)))
         return {"hwm": hwm.value, "skipped": sk.value, "overflow": ov.value}
+
+    def counters(self) -> dict:
+        """All device-side counters (synchronises the current stream): hwm, skipped, scan_overflow,
+        tc_fallbacks (batched-path users recomputed exactly on the device)."""
+        c = _Counters()
+        _check(library().linr_index_counters(self._h, ctypes.byref(c), _stream(self.device)))
+        return {f: getattr(c, f) for f, _ in _Counters._fields_}
 
     def profile(self, enable: bool = True):
         _check(library().linr_index_profile(self._h, 1 if enable else 0))
@@ -265,6 +380,7 @@ class Index:
         q = self._q(queries)
         B, V, _ = q.shape
         cl = clause_array(clauses)
+        assert cl.B == B, "one clause list per query"
         if out is None:
             keys = torch.empty((B, K), dtype=torch.int64, device=self.device)
             ps = torch.empty(B, dtype=torch.int64, device=self.device)
@@ -285,6 +401,7 @@ class Index:
         assert q.device.type == "cpu" and q.is_contiguous()
         B, V, _ = q.shape
         cl = clause_array(clauses)
+        assert cl.B == B, "one clause list per query"
         if out is None:
             ids = torch.empty((B, K), dtype=torch.int64, pin_memory=True)
             sc = torch.empty((B, K), dtype=torch.float32, pin_memory=True)
@@ -300,6 +417,13 @@ class Index:
                                           ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
                                           _stream(self.device)))
         return ids, sc, ps
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (linr_nccl_unique_id): create on one rank, broadcast to the others."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(library().linr_nccl_unique_id(ctypes.addressof(buf)))
+    return bytes(buf)
 
 
 def merge_keys(keys: torch.Tensor, pas: torch.Tensor, K: int, out=None):

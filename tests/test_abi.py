@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_error_string(L):
-    assert L.linr_version() == 1
+    assert L.linr_version() == 2
     assert isinstance(L.linr_last_error(), bytes)
 
 

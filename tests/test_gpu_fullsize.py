@@ -76,3 +76,9 @@ def test_c3_int8_shard_12p5M_high():
 def test_c4_int8_d64_shard_low():
     """c4-shaped shard (int8 d=64, 1B/8 rows would be 125M; 20M here), exact, LOW preset."""
     run_full(dg.I8, 64, 20_000_000, 1, 1, 1000, "LOW", dg.MODE_DENSE)
+
+
+def test_c2_bf16_10M_B256_dense_tcgen05():
+    """c2 at B=256 (the batched tcgen05 path bench.py times) on dense inputs: R8/R9 tolerance,
+    checked on sampled queries (first, middle, last) against the chunked oracle."""
+    run_full(dg.BF16, 128, 10_000_000, 256, 1, 1000, "HIGH", dg.MODE_DENSE, check_queries=[0, 101, 255])

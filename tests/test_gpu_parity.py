@@ -43,7 +43,7 @@ def test_config_c1_full():
 
 
 @pytest.mark.parametrize("dtype", [dg.F32, dg.F16, dg.BF16, dg.I8])
-@pytest.mark.parametrize("d", [16, 64, 128, 256])
+@pytest.mark.parametrize("d", [16, 32, 64, 128, 256, 512, 1024])
 def test_dtypes_dims_grid_exact(dtype, d):
     run_case(dtype, d, 20_011, 1, 1, 1000, "HIGH", dg.MODE_GRID, what=f"dt{dtype} d{d}")
 
@@ -309,7 +309,7 @@ def test_batched_tensor_core_path(dtype, d, B, V, K, preset, n):
     g = ix.search(to_torch(Q, dtype, DEV), cls, K)
     torch.cuda.synchronize()
     prof = ix.profile_read()
-    assert prof["launches"] == 5, prof   # sample, threshold, main, finalize, pass count: the tcgen05 path ran
+    assert prof["launches"] == 6, prof   # sample, threshold, main, finalize, fallback, pass count: the tcgen05 path ran
     ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what=f"tc dt{dtype} d{d} B{B} V{V}")
 
@@ -326,3 +326,130 @@ def test_kernel_variants(monkeypatch, env, dtype, d, B, V, preset):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     run_case(dtype, d, 300_000, B, V, 1000, preset, dg.MODE_GRID, what=f"variant {env}")
+
+
+@pytest.mark.parametrize("dtype,d,B,V,K,preset,n", [
+    (dg.BF16, 128, 64, 1, 1000, "HIGH", 150_000),
+    (dg.F16, 128, 32, 1, 200, "ALL", 60_000),
+    (dg.BF16, 64, 8, 4, 300, "HIGH4", 80_000),
+    (dg.F16, 64, 256, 1, 50, "HIGH", 40_000),
+])
+def test_batched_tensor_core_dense(dtype, d, B, V, K, preset, n):
+    """The tcgen05 path on dense (full-mantissa) inputs: scores rebuilt as acc + t_eff (reading R22)
+    must sit inside the R8 tolerance and the id sets obey R9."""
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_DENSE)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, dg.MODE_DENSE)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 6
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, False, what=f"tc dense dt{dtype} d{d} B{B} V{V}")
+
+
+@pytest.mark.parametrize("dtype,mode,d,B,V,K,preset", [
+    (dg.BF16, dg.MODE_GRID, 128, 32, 1, 500, "HIGH"),
+    (dg.I8, dg.MODE_DENSE, 64, 16, 1, 1000, "ALL"),
+    (dg.F16, dg.MODE_DENSE, 128, 8, 2, 100, "HIGH4"),
+    (dg.BF16, dg.MODE_GRID, 64, 4, 8, 2048, "LOW"),
+])
+def test_batched_certification_fallback_forced(monkeypatch, dtype, mode, d, B, V, K, preset):
+    """LINR_TC_MAIN_CAP shrinks the per-(user, CTA) candidate regions of the main pass so they
+    overflow: every affected user is flagged by the finalize kernel and recomputed exactly on the
+    device (fallback.cu, reading R23). The result must still equal the oracle, and the device
+    counter must show the recomputations."""
+    monkeypatch.setenv("LINR_TC_MAIN_CAP", "2")
+    n = 120_000
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    before = ix.counters()["tc_fallbacks"]
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    c = ix.counters()
+    assert c["tc_fallbacks"] - before > 0, c
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    exact = dtype == dg.I8 or mode == dg.MODE_GRID
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, exact, what=f"fallback dt{dtype} B{B} V{V}")
+    # keys form (shard-local search) takes the same fallback
+    k, ps = ix.search_keys(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    assert ix.counters()["tc_fallbacks"] > c["tc_fallbacks"]
+    from paper_2407_13218_b200 import merge_keys
+    g2 = merge_keys(k[None], ps[None], K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g2, ref, exact, what="fallback keys")
+
+
+def test_batched_fallback_not_taken_normally():
+    n, d, B, K = 200_000, 128, 64, 1000
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dg.BF16, dg.MODE_GRID)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    ix.search(to_torch(Q, dg.BF16, DEV), cls, K)
+    assert ix.counters()["tc_fallbacks"] == 0
+
+
+@pytest.mark.parametrize("B", [1, 64])
+def test_search_does_not_block_the_host(B):
+    """linr_search enqueues and returns (include/linr.h conventions): with a long spin kernel queued
+    ahead of it on the stream, the call returns while the stream is still busy -- on the GEMV path
+    and on the batched tcgen05 path (whose certification runs on the device)."""
+    n, d, K = 100_000, 128, 100
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dg.BF16, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dg.BF16)
+    Q = to_torch(dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dg.BF16, dg.MODE_GRID), dg.BF16, DEV)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    ix.search(Q, cls, K)   # warm-up: workspace allocation, attributes
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    torch.cuda._sleep(2_000_000_000)   # ~1 s of device time ahead of the search
+    ix.search(Q, cls, K)
+    busy = not s.query()
+    torch.cuda.synchronize()
+    assert busy, "linr_search synchronised the stream"
+
+
+@pytest.mark.parametrize("B,dtype,mode", [(2, dg.I8, dg.MODE_DENSE), (32, dg.BF16, dg.MODE_GRID)])
+def test_nccl_communicator_search_world1(B, dtype, mode):
+    """The library's own NCCL exchange (linr_nccl_unique_id + linr_comm_init; linr_search then packs
+    keys + pass counts, runs ncclAllGather and the merge kernel in the same call). One GPU here, so
+    the communicator has one rank: the branch runs end to end and must equal the oracle."""
+    from paper_2407_13218_b200 import nccl_unique_id
+    n, d, K = 90_000, 128, 700
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    ix.attach_comm(nccl_unique_id(), 0, 1)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what=f"nccl B{B}")
+    qh = torch.from_numpy(np.ascontiguousarray(Q).view(np.int16 if dtype != dg.I8 else np.int8))
+    if dtype == dg.BF16:
+        qh = qh.view(torch.bfloat16)
+    g2 = ix.search_host(qh.contiguous().pin_memory(), cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g2, ref, True, what=f"nccl host B{B}")
+
+
+def test_update_duplicate_ids_last_writer_wins():
+    """an id repeated within one update call is written by its last occurrence only."""
+    n, d, K = 5_000, 64, 50
+    vals, attrs = dg.gen_items(1, 0, n, d, dg.I8)
+    ix = make_index(vals, attrs, dg.I8)
+    rows = np.array([7, 9, 7, 7, 100, 9], np.int64)
+    nv, na = dg.gen_items(2, 0, len(rows), d, dg.I8)
+    ix.update_rows(torch.from_numpy(rows).to(DEV), to_torch(nv, dg.I8, DEV), attrs_torch(na, DEV))
+    fv, fa = vals.copy(), attrs.copy()
+    for j, r in enumerate(rows):   # sequential application == last writer wins
+        fv[r], fa[r] = nv[j], na[j]
+    Q = dg.gen_queries(3, 1, n, 2, 1, d, dg.I8)
+    cls = [[], [(0xFF << 56, 0, 0)]]
+    g = ix.search(to_torch(Q, dg.I8, DEV), cls, K)
+    ref = oracle.search(dg.I8, fv, fa, np.ones(n), Q, cls, K)
+    check(dg.I8, fv, fa, np.ones(n), Q, cls, K, g, ref, True, what="dup updates")
+    assert ix.emb_storage[:n * d].view(torch.int8).reshape(n, d)[7].cpu().numpy().tolist() == nv[3].tolist()

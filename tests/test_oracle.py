@@ -212,6 +212,27 @@ def test_grid_mode_scores_are_exact_integers(dtype):
     assert (s * 2.0 ** 14).tolist() == [float(v) for v in ref]
 
 
+def test_float_accumulation_is_fp64_cancellation():
+    """Reading R8: the oracle widens exactly and sums in fp64 (not fp32). Cancellation vectors fix
+    the precision: [2^24, 1, -2^24] . [1, 1, 1] is exactly 1; an fp32 running sum gives
+    fl32(2^24 + 1) - 2^24 = 0, and a sum in any other order than index order still differs
+    from the fp64 value for the second row (2^-30 below fp32 resolution at 1)."""
+    X = np.zeros((2, 16), np.float32)
+    X[0, :3] = [2.0 ** 24, 1.0, -(2.0 ** 24)]
+    X[1, :3] = [1.0, 2.0 ** -30, 2.0 ** -30]
+    q = np.zeros(16, np.float32)
+    q[:3] = 1.0
+    s = oracle.scores(oracle.F32, X, q)
+    assert s[0] == 1.0                       # fp32 accumulation would give 0.0
+    assert s[1] == 1.0 + 2.0 ** -29          # fp32 accumulation would give 1.0
+    # the same through the search (the definition the GPU is compared against)
+    ids, sc, _ = oracle.search(oracle.F32, X, np.ones((2, 1), np.uint64), np.ones(2), q[None], [[]], 2)
+    assert ids[0].tolist() == [1, 0] and sc[0].tolist() == [1.0 + 2.0 ** -29, 1.0]
+    # bf16 widening feeds the same fp64 sum: 2^24 and 1 are exact bf16 values
+    b = dg.f32_to_bf16_bits(X[:1])
+    assert oracle.scores(oracle.BF16, b, dg.f32_to_bf16_bits(q))[0] == 1.0
+
+
 def test_zero_query_returns_first_passing_ids():
     rng = np.random.default_rng(4)
     n, d = 200, 16

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the row-sharding host logic (-m "not gpu").
 
 What runs on CPU: shard_range partitioning, the key exchange (sharded.exchange over
-torch.distributed all_gather), update routing (sharded.route_rows). The per-shard top-K on each
+torch.distributed all_gather, keys and pass counts in one collective), single-owner update
+routing (sharded.route_rows / owner_of). The per-shard top-K on each
 rank comes from the oracle (no GPU here) packed into the ABI's u64 key format by this test; the
 gathered lists are merged with oracle.merge and must equal the oracle on the unsharded index
 (reading R13). The GPU side of the same path (linr_search_keys + linr_merge_keys) is covered by
@@ -18,7 +19,7 @@ import torch.multiprocessing as mp
 
 import datagen as dg
 import oracle
-from paper_2407_13218_b200.sharded import exchange, route_rows, shard_range
+from paper_2407_13218_b200.sharded import exchange, owner_of, route_rows, shard_range
 
 N, D, K, B = 6_000, 64, 50, 3
 
@@ -68,7 +69,7 @@ def _worker(rank, world, port, out):
         merged = oracle.merge(gids, gsc, gp.numpy(), K)
         # update routing: every rank sees the same replicated batch, keeps only its rows
         rows = torch.tensor([0, per - 1, per, N - 1, N + 5, -1])
-        mine = rows[route_rows(rows, lo, hi)].tolist()
+        mine = rows[route_rows(rows, rank, per, world)].tolist()
         out.put((rank, [m.tolist() for m in merged], mine, (lo, hi)))
     finally:
         dist.destroy_process_group()
@@ -103,7 +104,13 @@ def test_sharded_exchange_and_merge_gloo(world):
         assert np.array_equal(np.array(merged[0]), full[0]), rank
         assert np.array_equal(np.array(merged[1]), full[1]), rank
         assert np.array_equal(np.array(merged[2]), full[2]), rank
-        assert mine == [r for r in [0, per - 1, per, N - 1, N + 5, -1] if lo <= r < hi]
+        # single owner per id: [r*per, (r+1)*per), the last rank also takes growth rows, rank 0 the
+        # invalid negative ids (skipped and counted on the device)
+        rows = [0, per - 1, per, N - 1, N + 5, -1]
+        want = [r for r in rows if min(max(r // per, 0), world - 1) == rank]
+        assert mine == want
+    owned = sorted(sum((m for _, _, m, _ in res), []))
+    assert owned == sorted([0, per - 1, per, N - 1, N + 5, -1])   # every id routed exactly once
 
 
 def test_key_packing_roundtrip_and_order():
@@ -126,3 +133,17 @@ def test_shard_range_covers_exactly():
                 assert hi - lo <= per
                 cov.extend(range(lo, hi))
             assert cov == list(range(n))
+
+
+def test_owner_routing_is_unique_with_empty_shards():
+    """shard_range(10, 8) used to give ranks 5-7 the same lo (overlapping routing)."""
+    n, g = 10, 8
+    los = [shard_range(n, g, r)[0] for r in range(g)]
+    assert los == sorted(set(los))                  # disjoint, ordered
+    rows = torch.arange(-3, 40)
+    own = owner_of(rows, shard_range(n, g, 0)[2], g)
+    for r in range(g):
+        sel = route_rows(rows, r, shard_range(n, g, 0)[2], g)
+        assert torch.equal(own[sel], torch.full_like(sel, r))
+    counts = sum(route_rows(rows, r, 2, g).numel() for r in range(g))
+    assert counts == rows.numel()                   # each id goes to exactly one rank

@@ -1111,7 +1111,7 @@ namespace {
 constexpr int kCodeWarps = 16;   // warps per code-scan CTA (codes.cu kCodeNW)
 
 struct CodeWs {
-  size_t q, cl, kept, pass, mstar, T, H, off, marr, tmax, cand, lists, end;
+  size_t q, cl, kept, pass, mstar, T, H, off, marr, tmax, cand, lists, above, end;
   int g;   // users per launch group
 };
 
@@ -1119,7 +1119,7 @@ int code_group(const linr_index* ix, int B, int V) {
   const int K1 = ix->code_k + 1;
   int g = std::min(B, kCodeMaxUsers);
   while (g > 1 && (code_hist_smem(g, V, ix->code_k) > ix->smem_optin ||
-                   (size_t)kCodeWarps * g * K1 * 4 > ix->smem_optin))
+                   (size_t)kCodeWarps * 3072 + (size_t)kCodeWarps * g * K1 * 4 > ix->smem_optin))
     --g;
   return g;
 }
@@ -1135,8 +1135,9 @@ CodeWs code_layout(const linr_index* ix, int B, int V, int64_t K, bool v3) {
   w.kept = w.cl + align256((size_t)B * 16 * sizeof(KClause) + (size_t)B * 4);
   w.pass = w.kept + align256((size_t)B * 8);
   w.mstar = w.pass + align256((size_t)B * 8);
-  w.T = w.mstar + align256((size_t)g * 4);
-  w.H = w.T + align256((size_t)g * K1 * 8);
+  w.T = w.mstar + align256((size_t)g * 4);          // T [g][K1] u64 followed by the ticket (one memset)
+  w.above = w.T + align256((size_t)g * K1 * 8 + 8);
+  w.H = w.above + align256((size_t)g * (K1 + 1) * 8);
   w.off = w.H + align256((size_t)g * GW * K1 * 4);
   w.marr = w.off + align256((size_t)g * GW * K1 * 4);
   w.tmax = w.marr + align256((size_t)g * ix->cap_pad * msz);
@@ -1183,7 +1184,7 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     uint32_t wmask = 0;
     for (int b = u0; b < u0 + g; ++b)
       for (int c = off[b]; c < off[b + 1]; ++c) wmask |= 1u << cl[c].word;
-    e = cudaMemsetAsync(W + w.T, 0, (size_t)g * K1 * 8, st);
+    e = cudaMemsetAsync(W + w.T, 0, (size_t)g * K1 * 8 + 8, st);
     if (e != cudaSuccess) return cuda_fail(e, "code totals reset");
     CodeScanParams sp;
     std::memset(&sp, 0, sizeof(sp));
@@ -1203,19 +1204,35 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     sp.tmax_stride = ix->cap_pad / 256;
     sp.H = (uint32_t*)(W + w.H);
     sp.T = (unsigned long long*)(W + w.T);
+    sp.ticket = (unsigned int*)(W + w.T + (size_t)g * K1 * 8);
+    sp.K = K;
+    sp.keep = keep;
+    sp.mstar = (int*)(W + w.mstar);
+    sp.kept = kept + u0;
+    sp.pass = pass + u0;
+    sp.above = (unsigned long long*)(W + w.above);
+    ProfEvents pe{};
+    if (ix->prof) {   // stage timing: pass 1 (the dominant kernel) vs the rest of the pipeline
+      if (!ix->prof_free.empty()) {
+        pe = ix->prof_free.back();
+        ix->prof_free.pop_back();
+      } else {
+        cudaEventCreate(&pe.e0);
+        cudaEventCreate(&pe.e1);
+        cudaEventCreate(&pe.e2);
+      }
+      cudaEventRecord(pe.e0, st);
+    }
     e = launch_code_hist(ix->code_k, sp, ix->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "code pass 1 launch");
+    if (ix->prof) cudaEventRecord(pe.e1, st);
     CodeOffsetParams op;
     op.H = sp.H;
-    op.T = sp.T;
+    op.above = sp.above;
+    op.mstar = sp.mstar;
     op.GW = GW;
     op.k = ix->code_k;
-    op.K = K;
-    op.keep = keep;
     op.off = (uint32_t*)(W + w.off);
-    op.mstar = (int*)(W + w.mstar);
-    op.kept = kept + u0;
-    op.pass = pass + u0;
     e = launch_code_offsets(op, g, st);
     if (e != cudaSuccess) return cuda_fail(e, "code offsets launch");
     CodeEmitParams ep;
@@ -1228,8 +1245,8 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     ep.row0 = (uint32_t)ix->d.global_row0;
     ep.nu = g;
     ep.off = op.off;
-    ep.mstar = op.mstar;
-    ep.kept = op.kept;
+    ep.mstar = sp.mstar;
+    ep.kept = sp.kept;
     if (v3) {
       ep.out_stride = ix->cap_pad;
       ep.cand = (uint32_t*)(W + w.cand);
@@ -1241,8 +1258,13 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     e = launch_code_emit(ix->code_k, ep, ix->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "code pass 2 launch");
     if (!v3) {
-      e = launch_code_pad(op.kept, g, K, ep.out_ids, ep.out_m, ix->num_sms * 4, st);
+      e = launch_code_pad(sp.kept, g, K, ep.out_ids, ep.out_m, ix->num_sms * 4, st);
       if (e != cudaSuccess) return cuda_fail(e, "code pad launch");
+      if (ix->prof) {
+        cudaEventRecord(pe.e2, st);
+        ix->prof_used.push_back(pe);
+        ix->prof_launches += 4;   // pass 1, offsets, pass 2, pad
+      }
       continue;
     }
     RerankParams rp;
@@ -1256,7 +1278,7 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     rp.q = (const char*)q + (size_t)u0 * V * ix->rowbytes;
     rp.cand = ep.cand;
     rp.cand_stride = ix->cap_pad;
-    rp.kept = op.kept;
+    rp.kept = sp.kept;
     rp.lists = (uint64_t*)(W + w.lists);
     e = launch_rerank(ix->d.dtype, rp, ix->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "rerank launch");
@@ -1278,7 +1300,13 @@ int code_pipeline(linr_index* ix, const void* q, int B, int V, const linr_clause
     mp.dbg = debug_buffer();
     e = launch_merge(mp, g, st);
     if (e != cudaSuccess) return cuda_fail(e, "rerank merge launch");
+    if (ix->prof) {
+      cudaEventRecord(pe.e2, st);
+      ix->prof_used.push_back(pe);
+      ix->prof_launches += 5;   // pass 1, offsets, pass 2, rerank, merge
+    }
   }
+  if (ix->prof) ix->prof_launches += 1;   // the query encoding
   if (out_kept) {
     e = cudaMemcpyAsync(out_kept, kept, (size_t)B * 8, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "kept copy");

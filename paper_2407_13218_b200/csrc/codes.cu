@@ -32,6 +32,8 @@
 #include "common.cuh"
 #include "internal.h"
 
+#define LINR_DEV_HOST_INLINE __host__ __device__ __forceinline__
+
 namespace linr {
 
 constexpr int kCodeNT = 512;
@@ -79,10 +81,49 @@ __global__ void __launch_bounds__(256) oporp_encode_kernel(const void* __restric
   codes[(size_t)r * words + w] = code;
 }
 
+// Few vectors (the queries of a search): one warp per (vector, 32 bins), lane = bin, so the
+// per-bin sums run in parallel (the per-word kernel above serialises 64 bins per thread); the
+// warp's 32 bits are one ballot. Same fp64 position-order sums, same bits.
+template <int DT>
+__global__ void __launch_bounds__(256) oporp_encode_bins_kernel(const void* __restrict__ x, int dim, int64_t n, int k,
+                                                                int L, const int32_t* __restrict__ src,
+                                                                const int8_t* __restrict__ sign, uint32_t* codes32) {
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int groups = k >> 5;
+  const int64_t i = gwarp / groups;
+  if (i >= n) return;   // warp-uniform
+  const int g = (int)(gwarp - i * groups);
+  const int b = L / k;
+  const int p0 = (g * 32 + lane) * b;
+  const size_t xo = (size_t)i * dim;
+  double s = 0.0;
+  for (int p = p0; p < p0 + b; ++p) {
+    const int c = __ldg(src + p);
+    const double v = c < 0 ? 0.0 : code_elem<DT>(x, xo + c);
+    s = __dadd_rn(s, __ldg(sign + p) > 0 ? v : -v);
+  }
+  const uint32_t bits = __ballot_sync(0xffffffffu, s >= 0.0);
+  if (lane == 0) codes32[i * groups + g] = bits;   // LSB-first: bins 32g..32g+31 = u32 half g
+}
+
 cudaError_t launch_oporp_encode(int dtype, const void* x, int dim, int64_t n, int64_t row_begin, const int64_t* rows,
                                 int64_t grow0, int64_t cap, int k, int L, const int32_t* src, const int8_t* sign,
                                 uint64_t* codes, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (!rows && row_begin == 0 && n * (int64_t)k <= (1 << 22)) {
+    const int64_t threads = n * k;
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(codes);
+    switch (dtype) {
+      case LINR_F32: oporp_encode_bins_kernel<LINR_F32><<<blocks, 256, 0, st>>>(x, dim, n, k, L, src, sign, c32); break;
+      case LINR_F16: oporp_encode_bins_kernel<LINR_F16><<<blocks, 256, 0, st>>>(x, dim, n, k, L, src, sign, c32); break;
+      case LINR_BF16: oporp_encode_bins_kernel<LINR_BF16><<<blocks, 256, 0, st>>>(x, dim, n, k, L, src, sign, c32); break;
+      case LINR_I8: oporp_encode_bins_kernel<LINR_I8><<<blocks, 256, 0, st>>>(x, dim, n, k, L, src, sign, c32); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   const int64_t threads = n * (k / 64);
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   switch (dtype) {
@@ -95,6 +136,29 @@ cudaError_t launch_oporp_encode(int dtype, const void* x, int dim, int64_t n, in
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ bulk-copy (TMA) helpers
+LINR_DEV uint32_t cs_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+LINR_DEV void cs_mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cs_u32(b)), "r"(count) : "memory");
+}
+LINR_DEV void cs_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cs_u32(b)), "r"(bytes) : "memory");
+}
+LINR_DEV void cs_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tCS_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 2000;\n\t"
+      "@P1 bra CS_DONE;\n\tbra CS_WAIT;\n\tCS_DONE:\n\t}" ::"r"(cs_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+LINR_DEV void cs_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   cs_u32(dst)),
+               "l"(src), "r"(bytes), "r"(cs_u32(bar))
+               : "memory");
+}
+
 // ------------------------------------------------------------------ pass 1: filter + matched bits + histograms
 template <int WORDS>
 struct CodeGeom {
@@ -103,25 +167,40 @@ struct CodeGeom {
   static constexpr int IB = WORDS <= 2 ? 8 : (WORDS <= 4 ? 4 : (WORDS <= 8 ? 2 : 1));   // items per load batch
 };
 
+// lane-private u16 histograms (no atomics, no conflicts) when one user's k+1 bins x 32 lanes fit
+LINR_DEV_HOST_INLINE bool code_lanepriv(int nu, int k) { return nu == 1 && k <= 64; }
+constexpr int kCodeStages = 3;                        // per-warp bulk-copy ring: attribute word 0 + liveness
+constexpr int kCodeStageBytes = 256 * 8 + 32;         // of one 256-item tile
 size_t code_hist_smem(int nu, int V, int k) {
   const size_t h = ((size_t)kCodeNW * nu * (k + 1) * 4 + 15) & ~size_t(15);
+  const size_t lp = code_lanepriv(nu, k) ? (size_t)kCodeNW * (k + 1) * 32 * 2 : 0;
   const size_t q = ((size_t)nu * V * (k / 64) * 8 + 15) & ~size_t(15);
   const size_t t = (size_t)kCodeNW * nu * 256 * (k <= 192 ? 1 : 2);
-  return h + q + t + 16;
+  const size_t ring = (size_t)kCodeNW * kCodeStages * kCodeStageBytes + (size_t)kCodeNW * kCodeStages * 8;
+  return h + lp + q + t + ring + 32;
 }
 
-template <int WORDS>
+template <int WORDS, int NUM>
 __global__ void __launch_bounds__(kCodeNT, 1) code_hist_kernel(const __grid_constant__ CodeScanParams p) {
   using Gm = CodeGeom<WORDS>;
   using MT = typename Gm::MT;
   extern __shared__ __align__(16) unsigned char csm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nu = p.nu, V = p.V, K1 = WORDS * 64 + 1;
+  const int nu = NUM == 1 ? 1 : p.nu, V = p.V, K1 = WORDS * 64 + 1;   // NUM: users compiled for (1 or 8)
   uint32_t* hist = reinterpret_cast<uint32_t*>(csm);   // [NW][nu][K1]
-  uint64_t* snq = reinterpret_cast<uint64_t*>(csm + (((size_t)kCodeNW * nu * K1 * 4 + 15) & ~size_t(15)));   // [nu][V][WORDS]
+  const bool lp = WORDS <= 2 && code_lanepriv(nu, WORDS * 64);
+  uint16_t* lh = reinterpret_cast<uint16_t*>(csm + (((size_t)kCodeNW * nu * K1 * 4 + 15) & ~size_t(15)));   // [NW][K1][32]
+  uint64_t* snq = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(lh) +
+                                              (lp ? (size_t)kCodeNW * K1 * 32 * 2 : 0));   // [nu][V][WORDS]
   MT* stile = reinterpret_cast<MT*>(reinterpret_cast<unsigned char*>(snq) +
                                     (((size_t)nu * V * WORDS * 8 + 15) & ~size_t(15)));   // [NW][nu][256], 16B-aligned
+  unsigned char* ring = reinterpret_cast<unsigned char*>(stile) + (size_t)kCodeNW * nu * 256 * sizeof(MT);   // 16B-aligned
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(ring + (size_t)kCodeNW * kCodeStages * kCodeStageBytes);
   for (int i = tid; i < kCodeNW * nu * K1; i += kCodeNT) hist[i] = 0u;
+  if (lp)
+    for (int i = tid; i < kCodeNW * K1 * 16; i += kCodeNT) reinterpret_cast<uint32_t*>(lh)[i] = 0u;
+  if (tid < kCodeNW * kCodeStages) cs_mbar_init(&rbar[tid], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   for (int i = tid; i < nu * V * WORDS; i += kCodeNT) snq[i] = ~p.qcodes[i];   // NOT(query code), Fig. 3
   __syncthreads();
   const int gw = blockIdx.x * kCodeNW + warp, GW = gridDim.x * kCodeNW;
@@ -129,28 +208,67 @@ __global__ void __launch_bounds__(kCodeNT, 1) code_hist_kernel(const __grid_cons
   const int64_t ntiles = (hwm + 255) / 256;
   const int64_t t0 = ntiles * gw / GW, t1 = ntiles * (gw + 1) / GW;
   uint32_t* myhist = hist + (size_t)warp * nu * K1;
+  uint16_t* mylh = lh + (size_t)warp * K1 * 32 + lane;
   MT* mytile = stile + (size_t)warp * nu * 256;
   const bool w0 = (p.wmask & 1u) != 0;
-  uint64_t a[8], na[8];
-  uint32_t lw = 0, nlw = 0;
-  auto prefetch = [&](int64_t tile, uint64_t (&dst)[8], uint32_t& l) {
-    const int64_t base = tile * 256;
-    l = lane < 8 ? __ldg(p.live + (base >> 5) + lane) : 0u;
-    if (w0) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t) dst[t] = ldg_stream_u64(p.attr + base + t * 32 + lane);
+  // per-warp ring of kCodeStages tiles: attribute word 0 (2 KB) + liveness (32 B) of a tile arrive
+  // by one bulk copy each (TMA, no registers held while in flight); tile t uses stage (t - t0) % S
+  unsigned char* myring = ring + (size_t)warp * kCodeStages * kCodeStageBytes;
+  uint64_t* mybar = rbar + warp * kCodeStages;
+  auto issue = [&](int64_t tile) {
+    const int st = (int)((uint32_t)(tile - t0) % kCodeStages);
+    if (lane == 0) {
+      unsigned char* d = myring + st * kCodeStageBytes;
+      cs_mbar_expect_tx(&mybar[st], (w0 ? 2048u : 0u) + 32u);
+      if (w0) cs_bulk_load(d, p.attr + tile * 256, 2048u, &mybar[st]);
+      cs_bulk_load(d + 2048, p.live + tile * 8, 32u, &mybar[st]);
     }
   };
-  if (t0 < t1) prefetch(t0, a, lw);
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    if (tile + 1 < t1) prefetch(tile + 1, na, nlw);
+  auto fetch = [&](int64_t tile, uint64_t (&a)[8], uint32_t& lw) {   // wait for the tile's stage, read it
+    const uint32_t rel = (uint32_t)(tile - t0);
+    const int st = (int)(rel % kCodeStages);
+    cs_mbar_wait(&mybar[st], (rel / kCodeStages) & 1u);
+    const unsigned char* d = myring + st * kCodeStageBytes;
+    lw = lane < 8 ? reinterpret_cast<const uint32_t*>(d + 2048)[lane] : 0u;
+    if (w0) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = reinterpret_cast<const uint64_t*>(d)[t * 32 + lane];
+    }
+    __syncwarp();   // every lane has read the stage: it may be refilled
+    if (tile + kCodeStages < t1) issue(tile + kCodeStages);
+  };
+  // one tile: liveness + clauses, matched bits of the passing items, histogram, m array, tile max
+  // Software pipeline over the warp's tiles (k <= 128: codes of 8 B / 16 B per item): phase A of
+  // tile i+1 (liveness + clauses, then the predicated code loads) is issued before phase B of tile i
+  // (matched bits, histogram, m array), and the attributes of tile i+2 are in flight meanwhile; two
+  // register sets and a loop unrolled by two, so no register copy waits on an in-flight load.
+  constexpr bool kPipe = WORDS <= 2;
+  struct Stage {
+    uint32_t pb[NUM];
+    uint64_t c[kPipe ? 8 : 1][kPipe ? WORDS : 1];
+  };
+  auto load_code = [&](const uint64_t* cp, uint64_t* dst) {
+    if constexpr (WORDS == 1) {
+      dst[0] = ldg_stream_u64(cp);
+    } else {
+#pragma unroll
+      for (int q = 0; q < WORDS / 2; ++q) {
+        const uint4 v = ldg_stream_v4(cp + 2 * q);
+        dst[2 * q] = ((uint64_t)v.y << 32) | v.x;
+        dst[2 * q + 1] = ((uint64_t)v.w << 32) | v.z;
+      }
+    }
+  };
+  auto phaseA = [&](const int64_t tile, Stage& S) {
     const int64_t base = tile * 256;
+    uint64_t a[8];
+    uint32_t lw;
+    fetch(tile, a, lw);
     uint32_t mylive = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) mylive |= ((__shfl_sync(0xffffffffu, lw, t) >> lane) & 1u) << t;
-    uint32_t pb[kCodeMaxUsers];
 #pragma unroll
-    for (int u = 0; u < kCodeMaxUsers; ++u) pb[u] = u < nu ? mylive : 0u;
+    for (int u = 0; u < NUM; ++u) S.pb[u] = u < nu ? mylive : 0u;
     if (__any_sync(0xffffffffu, mylive != 0u)) {
 #pragma unroll 1
       for (int w = 0; w < 4; ++w) {
@@ -164,7 +282,7 @@ __global__ void __launch_bounds__(kCodeNT, 1) code_hist_kernel(const __grid_cons
           for (int t = 0; t < 8; ++t) aw[t] = ldg_stream_u64(p.attr + (size_t)w * p.cap_pad + base + t * 32 + lane);
         }
 #pragma unroll
-        for (int u = 0; u < kCodeMaxUsers; ++u) {
+        for (int u = 0; u < NUM; ++u) {
           if (u >= nu) continue;
           for (int c = 0; c < p.ncl[u]; ++c) {
             const KClause k = p.cl[u * 16 + c];
@@ -172,57 +290,65 @@ __global__ void __launch_bounds__(kCodeNT, 1) code_hist_kernel(const __grid_cons
             const bool rev = k.rev != 0u;
 #pragma unroll
             for (int t = 0; t < 8; ++t)
-              if (((aw[t] & k.mask) != 0ull) == rev) pb[u] &= ~(1u << t);
+              if (((aw[t] & k.mask) != 0ull) == rev) S.pb[u] &= ~(1u << t);
           }
         }
       }
     }
-    uint32_t anyp = 0;
+    if constexpr (kPipe) {   // codes of the passing items (predicated: sectors of non-passing items stay unread)
+      uint32_t anyp = 0;
 #pragma unroll
-    for (int u = 0; u < kCodeMaxUsers; ++u) anyp |= pb[u];
-    // codes of the passing items (predicated loads: sectors of non-passing items are not fetched)
+      for (int u = 0; u < NUM; ++u) anyp |= S.pb[u];
 #pragma unroll
-    for (int t0b = 0; t0b < 8; t0b += Gm::IB) {
-      uint64_t c[Gm::IB][WORDS];
+      for (int t = 0; t < 8; ++t)
+        if ((anyp >> t) & 1u) load_code(p.codes + (size_t)(base + t * 32 + lane) * WORDS, S.c[t]);
+    }
+  };
+  auto score = [&](const int t, const uint64_t* c, const Stage& S) {
+    const int it = t * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < Gm::IB; ++j) {
-        const int t = t0b + j;
-        if ((anyp >> t) & 1u) {
-          const uint64_t* cp = p.codes + (size_t)(base + t * 32 + lane) * WORDS;
-          if constexpr (WORDS == 1) {
-            c[j][0] = ldg_stream_u64(cp);
-          } else {
+    for (int u = 0; u < NUM; ++u) {
+      if (u >= nu) continue;
+      uint32_t m = Gm::kNone;
+      if ((S.pb[u] >> t) & 1u) {
+        int best = 0;
+        if (V == 1) {
+          const uint64_t* q = snq + (size_t)u * WORDS;
 #pragma unroll
-            for (int q = 0; q < WORDS / 2; ++q) {
-              const uint4 v = ldg_stream_v4(cp + 2 * q);
-              c[j][2 * q] = ((uint64_t)v.y << 32) | v.x;
-              c[j][2 * q + 1] = ((uint64_t)v.w << 32) | v.z;
-            }
+          for (int w = 0; w < WORDS; ++w) best += __popcll(q[w] ^ c[w]);
+        } else {
+          for (int v = 0; v < V; ++v) {
+            const uint64_t* q = snq + ((size_t)u * V + v) * WORDS;
+            int s = 0;
+#pragma unroll
+            for (int w = 0; w < WORDS; ++w) s += __popcll(q[w] ^ c[w]);
+            best = max(best, s);
           }
         }
+        m = (uint32_t)best;
+        if (lp) mylh[best * 32] += 1;   // this lane's own counter
+        else atomicAdd(&myhist[u * K1 + best], 1u);
       }
+      mytile[u * 256 + it] = (MT)m;
+    }
+  };
+  auto phaseB = [&](const int64_t tile, const Stage& S) {
+    const int64_t base = tile * 256;
+    if constexpr (kPipe) {
 #pragma unroll
-      for (int j = 0; j < Gm::IB; ++j) {
-        const int t = t0b + j;
-        const int it = t * 32 + lane;
+      for (int t = 0; t < 8; ++t) score(t, S.c[t], S);
+    } else {
+      uint32_t anyp = 0;
 #pragma unroll
-        for (int u = 0; u < kCodeMaxUsers; ++u) {
-          if (u >= nu) continue;
-          uint32_t m = Gm::kNone;
-          if ((pb[u] >> t) & 1u) {
-            int best = 0;
-            for (int v = 0; v < V; ++v) {
-              const uint64_t* q = snq + ((size_t)u * V + v) * WORDS;
-              int s = 0;
+      for (int u = 0; u < NUM; ++u) anyp |= S.pb[u];
 #pragma unroll
-              for (int w = 0; w < WORDS; ++w) s += __popcll(q[w] ^ c[j][w]);
-              best = max(best, s);
-            }
-            m = (uint32_t)best;
-            atomicAdd(&myhist[u * K1 + best], 1u);
-          }
-          mytile[u * 256 + it] = (MT)m;
-        }
+      for (int t0b = 0; t0b < 8; t0b += Gm::IB) {
+        uint64_t c[Gm::IB][WORDS];
+#pragma unroll
+        for (int j = 0; j < Gm::IB; ++j)
+          if ((anyp >> (t0b + j)) & 1u) load_code(p.codes + (size_t)(base + (t0b + j) * 32 + lane) * WORDS, c[j]);
+#pragma unroll
+        for (int j = 0; j < Gm::IB; ++j) score(t0b + j, c[j], S);
       }
     }
     __syncwarp();
@@ -245,72 +371,132 @@ __global__ void __launch_bounds__(kCodeNT, 1) code_hist_kernel(const __grid_cons
       if (lane == 0) p.tmax[(size_t)u * p.tmax_stride + tile] = mx < 0 ? (uint16_t)0xFFFFu : (uint16_t)mx;
     }
     __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 8; ++t) a[t] = na[t];
-    lw = nlw;
+  };
+  // pipeline: attributes + liveness kCodeStages tiles ahead (bulk copies), code loads two tiles
+  // ahead (phase A of tile i+2 before phase B of tile i), three register sets, unrolled by three
+  for (int64_t t = t0; t < t1 && t < t0 + kCodeStages; ++t) issue(t);
+  if constexpr (WORDS == 1) {
+    Stage S0, S1, S2;
+    if (t0 < t1) phaseA(t0, S0);
+    if (t0 + 1 < t1) phaseA(t0 + 1, S1);
+    for (int64_t tile = t0; tile < t1; tile += 3) {
+      if (tile + 2 < t1) phaseA(tile + 2, S2);
+      phaseB(tile, S0);
+      if (tile + 1 >= t1) break;
+      if (tile + 3 < t1) phaseA(tile + 3, S0);
+      phaseB(tile + 1, S1);
+      if (tile + 2 >= t1) break;
+      if (tile + 4 < t1) phaseA(tile + 4, S1);
+      phaseB(tile + 2, S2);
+    }
+  } else {   // wider codes: code loads one tile ahead (two register sets)
+    Stage S0, S1;
+    if (t0 < t1) phaseA(t0, S0);
+    for (int64_t tile = t0; tile < t1; tile += 2) {
+      if (tile + 1 < t1) phaseA(tile + 1, S1);
+      phaseB(tile, S0);
+      if (tile + 1 >= t1) break;
+      if (tile + 2 < t1) phaseA(tile + 2, S0);
+      phaseB(tile + 1, S1);
+    }
   }
   __syncwarp();
-  // per-warp histogram rows -> H[u][gw][K1]; CTA totals -> T[u][K1] (atomics)
+  if (lp) {   // fold the lane-private counters into the warp's histogram
+    const uint16_t* base = lh + (size_t)warp * K1 * 32;
+    for (int m = lane; m < K1; m += 32) {
+      uint32_t c = 0;
+      const uint32_t* r = reinterpret_cast<const uint32_t*>(base + (size_t)m * 32);
+#pragma unroll
+      for (int l = 0; l < 16; ++l) c += (r[l] & 0xFFFFu) + (r[l] >> 16);
+      myhist[m] = c;
+    }
+    __syncwarp();
+  }
+  // per-warp histograms -> H[u][K1][GW] (column m of every warp contiguous for the offset scans);
+  // CTA totals -> T[u][K1]
   for (int u = 0; u < nu; ++u)
-    for (int m = lane; m < K1; m += 32) p.H[((size_t)u * GW + gw) * K1 + m] = myhist[u * K1 + m];
+    for (int m = lane; m < K1; m += 32) p.H[((size_t)u * K1 + m) * GW + gw] = myhist[u * K1 + m];
   __syncthreads();
   for (int i = tid; i < nu * K1; i += kCodeNT) {
     unsigned long long s = 0;
     for (int w = 0; w < kCodeNW; ++w) s += hist[(size_t)w * nu * K1 + i];
     if (s) atomicAdd(&p.T[i], s);
   }
-}
-
-// ------------------------------------------------------------------ offsets: counts -> output positions
-__global__ void __launch_bounds__(1024) code_offsets_kernel(const __grid_constant__ CodeOffsetParams p) {
-  __shared__ unsigned long long sT[1025];
-  __shared__ unsigned long long s_above;
-  __shared__ int s_mstar;
-  __shared__ unsigned int wsum[32];
-  const int m = blockIdx.x, u = blockIdx.y, K1 = p.k + 1, tid = threadIdx.x;
-  for (int i = tid; i < K1; i += 1024) sT[i] = p.T[(size_t)u * K1 + i];
+  // the last CTA to finish turns the totals into the selection: per user the suffix counts
+  // S[m] = #items with m' >= m, the number of results kept = min(pass, K) (V3: min(pass,
+  // max(K, ceil(keep*pass)))), m* = the largest m with S[m] >= kept
+  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    unsigned long long pass = 0;
-    for (int i = 0; i < K1; ++i) pass += sT[i];
+  __shared__ unsigned int s_ticket;
+  if (tid == 0) s_ticket = atomicAdd(p.ticket, 1u);
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  __threadfence();
+  unsigned long long* S = reinterpret_cast<unsigned long long*>(csm);   // reuse: [K1 + 1]
+  for (int u = 0; u < nu; ++u) {
+    if (warp == 0) {   // suffix sums, lane l owns a contiguous chunk of the reversed bins
+      const int per = (K1 + 31) / 32;
+      unsigned long long loc = 0;
+      for (int j = 0; j < per; ++j) {
+        const int m = K1 - 1 - (lane * per + j);
+        if (m >= 0) loc += atomicAdd(&p.T[(size_t)u * K1 + m], 0ull);
+      }
+      unsigned long long incl = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      unsigned long long run = incl - loc;
+      for (int j = 0; j < per; ++j) {
+        const int m = K1 - 1 - (lane * per + j);
+        if (m >= 0) {
+          run += atomicAdd(&p.T[(size_t)u * K1 + m], 0ull);
+          S[m] = run;
+        }
+      }
+      if (lane == 0) S[K1] = 0ull;
+    }
+    __syncthreads();
+    const unsigned long long pass = S[0];
     unsigned long long want;
-    if (p.keep > 0.0) {   // V3: K' = min(pass, max(K, ceil(keep * pass)))
-      const double kd = ceil(p.keep * (double)pass);
-      unsigned long long kk = (unsigned long long)kd;
+    if (p.keep > 0.0) {
+      unsigned long long kk = (unsigned long long)ceil(p.keep * (double)pass);
       if (kk < (unsigned long long)p.K) kk = (unsigned long long)p.K;
       want = kk < pass ? kk : pass;
     } else {
       want = (unsigned long long)p.K < pass ? (unsigned long long)p.K : pass;
     }
-    // m* = the largest m with #(items with m' >= m) >= want (K1 when want == 0: nothing to emit)
-    int ms = K1;
-    unsigned long long cum = 0;
-    if (want > 0) {
-      for (int i = K1 - 1; i >= 0; --i) {
-        cum += sT[i];
-        if (cum >= want) { ms = i; break; }
-      }
-    }
-    unsigned long long above = 0;
-    for (int i = m + 1; i < K1; ++i) above += sT[i];
-    s_above = above;
-    s_mstar = ms;
-    if (m == 0) {
-      p.mstar[u] = ms;
+    if (tid == 0) {
+      p.mstar[u] = K1;   // nothing to emit unless a bin below qualifies
       p.kept[u] = (int64_t)want;
       if (p.pass) p.pass[u] = (int64_t)pass;
     }
+    __syncthreads();
+    for (int m = tid; m < K1; m += kCodeNT) {
+      p.above[(size_t)u * (K1 + 1) + m] = S[m + 1];
+      if (want > 0 && S[m] >= want && S[m + 1] < want) p.mstar[u] = m;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (m < s_mstar) return;
-  const unsigned long long above = s_above;
-  // exclusive scan over the warps' counts of value m (ordered by warp = by item id)
+  if (tid == 0) *p.ticket = 0u;   // reusable by the next search on this workspace
+}
+
+// ------------------------------------------------------------------ offsets: counts -> output positions
+// Block (m, u), m >= m*: exclusive scan over the warps (= item-id order) of their counts of value m,
+// offset by the number of items with a larger m: off[u][gw][m] = first output position of warp gw's
+// items with matched bits m.
+__global__ void __launch_bounds__(1024) code_offsets_kernel(const __grid_constant__ CodeOffsetParams p) {
+  __shared__ unsigned int wsum[32];
+  const int m = blockIdx.x, u = blockIdx.y, K1 = p.k + 1, tid = threadIdx.x;
+  if (m < p.mstar[u]) return;
+  const unsigned long long above = p.above[(size_t)u * (K1 + 1) + m];
   const int GW = p.GW;
   const int per = (GW + 1023) / 1024;
   const int g0 = tid * per;
+  const uint32_t* col = p.H + ((size_t)u * K1 + m) * GW;
   unsigned int loc = 0;
   for (int j = 0; j < per; ++j)
-    if (g0 + j < GW) loc += p.H[((size_t)u * GW + g0 + j) * K1 + m];
+    if (g0 + j < GW) loc += col[g0 + j];
   const int lane = tid & 31, wp = tid >> 5;
   unsigned int incl = loc;
   for (int o = 1; o < 32; o <<= 1) {
@@ -333,21 +519,32 @@ __global__ void __launch_bounds__(1024) code_offsets_kernel(const __grid_constan
   for (int j = 0; j < per; ++j) {
     const int g = g0 + j;
     if (g >= GW) break;
-    const unsigned int h = p.H[((size_t)u * GW + g) * K1 + m];
     p.off[((size_t)u * GW + g) * K1 + m] = (uint32_t)(run < 0xFFFFFFFFull ? run : 0xFFFFFFFFull);
-    run += h;
+    run += col[g];
   }
 }
 
 // ------------------------------------------------------------------ pass 2: emit in (m desc, id asc) order
+// Each warp walks its own tile range (the same as in pass 1) in id order. Tiles whose max m is below
+// m* are skipped (one tmax read per tile, 32 tiles per warp load); the m values of up to 2 KB of
+// qualifying tiles are loaded with 16-byte vector loads in one batch (memory-level parallelism),
+// staged in shared memory and read back item-major (item t*32 + lane), so the rank among equal m
+// (__match_any_sync) follows item ids.
 template <int WORDS>
 __global__ void __launch_bounds__(kCodeNT, 1) code_emit_kernel(const __grid_constant__ CodeEmitParams p) {
   using Gm = CodeGeom<WORDS>;
   using MT = typename Gm::MT;
+  constexpr int TB = 256 * (int)sizeof(MT);   // bytes of m per tile
+  constexpr int G = 2048 / TB;                // tiles per load batch
+  constexpr int LPT = TB / 16;                // lanes per tile load
+  constexpr int TPI = 32 / LPT;               // tiles per load instruction
+  constexpr int NI = G / TPI;                 // load instructions per batch
   extern __shared__ __align__(16) unsigned char esm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nu = p.nu, K1 = WORDS * 64 + 1;
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(esm);   // [NW][nu][K1]
+  unsigned char* mybuf = esm + (size_t)warp * 2048;
+  uint32_t* mylist = reinterpret_cast<uint32_t*>(esm + (size_t)kCodeNW * 2048) + (size_t)warp * 256;   // [NW][256]
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(esm + (size_t)kCodeNW * 3072);   // [NW][nu][K1]
   const int gw = blockIdx.x * kCodeNW + warp, GW = gridDim.x * kCodeNW;
   uint32_t* mycur = cursor + (size_t)warp * nu * K1;
   for (int u = 0; u < nu; ++u) {
@@ -362,36 +559,68 @@ __global__ void __launch_bounds__(kCodeNT, 1) code_emit_kernel(const __grid_cons
     const uint32_t ms = (uint32_t)p.mstar[u];
     const int64_t kept = p.kept[u];
     if ((int)ms >= K1 || kept == 0) continue;
-    const MT* marr = reinterpret_cast<const MT*>(p.marr) + (size_t)u * p.cap_pad;
+    const unsigned char* marr = reinterpret_cast<const unsigned char*>(p.marr) + (size_t)u * p.cap_pad * sizeof(MT);
     uint32_t* cu = mycur + u * K1;
-    for (int64_t tile = t0; tile < t1; ++tile) {
-      const uint32_t tm = p.tmax[(size_t)u * p.tmax_stride + tile];
-      if (tm == 0xFFFFu || tm < ms) continue;   // no candidate in this tile
-      const int64_t base = tile * 256;
-      uint32_t mv[8];
+    for (int64_t chunk = t0; chunk < t1; chunk += 32) {
+      const int64_t tl = chunk + lane;
+      const uint32_t tm = tl < t1 ? p.tmax[(size_t)u * p.tmax_stride + tl] : 0xFFFFu;
+      uint32_t q = __ballot_sync(0xffffffffu, tm != 0xFFFFu && tm >= ms);
+      while (q) {
+        const int ng = min(__popc(q), G);
+        uint4 v[NI];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) mv[t] = marr[base + t * 32 + lane];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t m = mv[t];
-        const bool cand = m != Gm::kNone && m >= ms;
-        if (__ballot_sync(0xffffffffu, cand) == 0u) continue;
-        const uint32_t peers = __match_any_sync(0xffffffffu, cand ? m : 0xFFFFFFFFu);
-        uint32_t pos = 0;
-        if (cand) {
-          pos = cu[m] + (uint32_t)__popc(peers & lanemask_lt());
-          if ((int64_t)pos < kept) {
-            const int64_t at = (int64_t)u * p.out_stride + pos;
-            const uint32_t lr = (uint32_t)(base + t * 32 + lane);
-            if (p.out_ids) {
-              p.out_ids[at] = (int64_t)(p.row0 + lr);
-              p.out_m[at] = (int32_t)m;
-            }
-            if (p.cand) p.cand[at] = lr;
+        for (int i = 0; i < NI; ++i) {
+          const int g = i * TPI + lane / LPT;
+          if (g < ng) {
+            const int j = (int)__fns(q, 0, g + 1);
+            v[i] = ldg_stream_v4(marr + (size_t)(chunk + j) * TB + (lane % LPT) * 16);
           }
         }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int g = i * TPI + lane / LPT;
+          if (g < ng) *reinterpret_cast<uint4*>(mybuf + g * TB + (lane % LPT) * 16) = v[i];
+        }
         __syncwarp();
-        if (cand && lane == 31 - __clz(peers)) cu[m] += (uint32_t)__popc(peers);
+        for (int g = 0; g < ng; ++g) {
+          const int j = __ffs(q) - 1;
+          q &= q - 1u;
+          const int64_t base = (chunk + j) * 256;
+          const MT* row = reinterpret_cast<const MT*>(mybuf + g * TB);
+          // candidates of the tile, compacted in item order (t-major, lane-minor = id order)
+          int nc = 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t m = row[t * 32 + lane];
+            const bool cand = m != Gm::kNone && m >= ms;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+            if (cand) mylist[nc + __popc(bal & lanemask_lt())] = ((uint32_t)(t * 32 + lane) << 16) | m;
+            nc += __popc(bal);
+          }
+          __syncwarp();
+          // 32 candidates at a time: rank among equal m by one match, positions from the cursors
+          for (int c0 = 0; c0 < nc; c0 += 32) {
+            const bool valid = c0 + lane < nc;
+            const uint32_t e = valid ? mylist[c0 + lane] : 0xFFFFFFFFu;
+            const uint32_t m = e & 0xFFFFu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? m : 0xFFFFFFFFu);
+            if (valid) {
+              const uint32_t pos = cu[m] + (uint32_t)__popc(peers & lanemask_lt());
+              if ((int64_t)pos < kept) {
+                const int64_t at = (int64_t)u * p.out_stride + pos;
+                const uint32_t lr = (uint32_t)(base + (e >> 16));
+                if (p.out_ids) {
+                  p.out_ids[at] = (int64_t)(p.row0 + lr);
+                  p.out_m[at] = (int32_t)m;
+                }
+                if (p.cand) p.cand[at] = lr;
+              }
+            }
+            __syncwarp();
+            if (valid && lane == 31 - __clz(peers)) cu[m] += (uint32_t)__popc(peers);
+            __syncwarp();
+          }
+        }
         __syncwarp();
       }
     }
@@ -516,7 +745,7 @@ size_t rerank_smem(int V, int dim) {
 template <int WORDS>
 static cudaError_t launch_hist_w(const CodeScanParams& p, int grid, cudaStream_t st) {
   const size_t smem = code_hist_smem(p.nu, p.V, WORDS * 64);
-  auto k = code_hist_kernel<WORDS>;
+  auto k = p.nu == 1 ? code_hist_kernel<WORDS, 1> : code_hist_kernel<WORDS, kCodeMaxUsers>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kCodeNT, smem, st>>>(p);
@@ -540,7 +769,7 @@ cudaError_t launch_code_offsets(const CodeOffsetParams& p, int nu, cudaStream_t 
 
 template <int WORDS>
 static cudaError_t launch_emit_w(const CodeEmitParams& p, int grid, cudaStream_t st) {
-  const size_t smem = (size_t)kCodeNW * p.nu * (WORDS * 64 + 1) * 4;
+  const size_t smem = (size_t)kCodeNW * 3072 + (size_t)kCodeNW * p.nu * (WORDS * 64 + 1) * 4;
   auto k = code_emit_kernel<WORDS>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;

@@ -196,19 +196,22 @@ struct CodeScanParams {            // pass 1: filter + matched bits + histograms
   void* marr;                      // [nu][cap_pad] u8 (k <= 192) / u16 matched bits, none = 0xFF / 0xFFFF
   uint16_t* tmax;                  // [nu][tmax_stride] per-tile max m (0xFFFF: no passing item)
   int64_t tmax_stride;
-  uint32_t* H;                     // [nu][GW][k+1] per-warp histograms
+  uint32_t* H;                     // [nu][k+1][GW] per-warp histograms
   unsigned long long* T;           // [nu][k+1] totals (zeroed before the launch)
-};
-struct CodeOffsetParams {
-  const uint32_t* H;
-  const unsigned long long* T;
-  int GW, k;
+  unsigned int* ticket;            // CTA completion counter (zeroed before; reset by the last CTA)
   int64_t K;                       // results wanted (code search) / the K floor of V3
   double keep;                     // > 0: V3 keep fraction
+  int* mstar;                      // [nu] out: the lowest m emitted (k+1: nothing)
+  int64_t* kept;                   // [nu] out: positions to produce
+  int64_t* pass;                   // [nu] out: passing items (may be null)
+  unsigned long long* above;       // [nu][k+2] out: #items with a larger m
+};
+struct CodeOffsetParams {
+  const uint32_t* H;               // [nu][k+1][GW]
+  const unsigned long long* above; // [nu][k+2]
+  const int* mstar;                // [nu]
+  int GW, k;
   uint32_t* off;                   // [nu][GW][k+1] first output position (valid for m >= m*)
-  int* mstar;                      // [nu]
-  int64_t* kept;                   // [nu] positions to produce
-  int64_t* pass;                   // [nu] passing items (may be null)
 };
 struct CodeEmitParams {
   const void* marr;

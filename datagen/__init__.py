@@ -27,6 +27,8 @@ UPDATE_SEED = 0x4429
 
 # counter streams
 S_CLUSTER, S_CENTER, S_NOISE, S_ATTR, S_QROW, S_QNOISE, S_QCLAUSE, S_OPORP = 1, 2, 3, 4, 5, 6, 7, 8
+S_IDL, S_IDVAL, S_QIDL = 9, 10, 11
+ID_SENTINEL = np.uint64(0xFFFFFFFFFFFFFFFF)   # padding of ID-list rows
 OPORP_SEED = 0x4294   # PAPER.md P:4294 (Sign-OPORP)
 
 N_CLUSTERS = 1024
@@ -341,3 +343,44 @@ def oporp_params(seed: int, d: int, k: int):
         perm[i], perm[j] = perm[j], perm[i]
     sgn = np.where((h1(seed, S_OPORP + 16, np.arange(L, dtype=U64)) & U64(1)) == U64(1), 1, -1).astype(np.int8)
     return perm.astype(np.int32), sgn
+
+
+# ---------------------------------------------------------------- ID-list attributes
+def id_of(seed: int, values) -> np.ndarray:
+    """64-bit attribute id of an attribute value (P:4564: attributes "converted to 64-bit integers");
+    never the padding sentinel."""
+    h = h1(seed, S_IDVAL, np.asarray(values, dtype=U64))
+    return np.where(h == ID_SENTINEL, U64(0), h)
+
+
+def gen_idlists(seed: int, row_begin: int, n: int, slot: int, A: int, universe: int, raw: bool = False):
+    """One ID-list slot for rows [row_begin, row_begin+n): ids [n][A] uint64 (each row's distinct ids
+    sorted ascending, padded with ID_SENTINEL) and counts [n] uint8 in [1, A]. Row r draws
+    1 + h % A values uniformly from [0, universe); raw=True keeps the values themselves as ids."""
+    rows = np.arange(row_begin, row_begin + n, dtype=U64)
+    hc = h2(seed, S_IDL, rows, U64(slot * 64))
+    want = (hc % U64(A)).astype(np.int64) + 1
+    vals = np.stack([(h2(seed, S_IDL, rows, U64(slot * 64 + 1 + a)) % U64(universe)) for a in range(A)], axis=1)
+    ids = vals.astype(U64) if raw else id_of(seed, vals)
+    out = np.full((n, A), ID_SENTINEL, dtype=U64)
+    cnt = np.zeros(n, dtype=np.uint8)
+    for i in range(n):
+        u = np.unique(ids[i, :want[i]])   # sorted, distinct
+        out[i, :len(u)] = u
+        cnt[i] = len(u)
+    return out, cnt
+
+
+def gen_id_clauses(qseed: int, dseed: int, B: int, slot: int, A: int, universe: int, nq: int, n_items: int,
+                   reverse: int = 0, raw: bool = False):
+    """Per query one ID-list clause on `slot`: the first value of a random item's list plus nq-1 random
+    values, as sorted distinct 64-bit ids. Returns [[(slot, reverse, ids)], ...]."""
+    out = []
+    for b in range(B):
+        src = int(h2(qseed, S_QIDL, U64(b), U64(slot)) % U64(max(1, n_items)))
+        first = int(h2(dseed, S_IDL, U64(src), U64(slot * 64 + 1)) % U64(universe))
+        others = [int(h2(qseed, S_QIDL, U64(b), U64(slot * 64 + 1 + j)) % U64(universe)) for j in range(nq - 1)]
+        vals = np.array([first] + others, dtype=U64)
+        ids = vals if raw else id_of(dseed, vals)
+        out.append([(slot, reverse, np.unique(ids))])
+    return out

@@ -68,6 +68,8 @@ def lib():
         L.oracle_search_v3.argtypes = [I, I, I64, I64, P, P, I, P, P, I, I, P, P, I, ctypes.c_double, I, I, P, P,
                                        P, P, P, P]
         L.oracle_search_v3.restype = I
+        L.oracle_search_idc.argtypes = [I, I, I64, I64, P, P, I, P, I, P, P, P, P, I, I, P, P, P, P, I, P, P, P]
+        L.oracle_search_idc.restype = I
         _lib = L
     return _lib
 
@@ -235,3 +237,58 @@ def search_v3(dtype, emb, attrs, live, queries, clauses, K, keep, k, prm, row0=0
     if rc != 0:
         raise ValueError("oracle precondition violated")
     return ids, sc, ps, kept
+
+
+# ---------------------------------------------------------------- ID-list clauses (linr_oracle.cpp)
+ID_CLAUSE_DTYPE = np.dtype([("ids", "<u8"), ("n", "<i4"), ("slot", "u1"), ("reverse", "u1"), ("pad", "u1", 2)])
+
+
+def search_idc(dtype, emb, attrs, live, idlists, queries, clauses, id_clauses, K, row0=0):
+    """Filtered top-K with bitmask clauses and ID-list clauses.
+    idlists: list over slots of (ids [n][A_s] uint64, counts [n] uint8);
+    id_clauses: per query, list of (slot, reverse, sorted query ids)."""
+    emb = np.ascontiguousarray(emb)
+    attrs = np.ascontiguousarray(attrs, dtype=np.uint64)
+    n, d = emb.shape
+    live = np.ascontiguousarray(live, dtype=np.uint8)
+    q = np.ascontiguousarray(queries)
+    if q.ndim == 2:
+        q = q[:, None, :]
+    B, V, _ = q.shape
+    ca, off = csr(clauses)
+    if len(ca) == 0:
+        ca = np.zeros(1, dtype=CLAUSE_DTYPE)
+    S = len(idlists)
+    keep = []
+    sid = (ctypes.c_void_p * max(1, S))()
+    scnt = (ctypes.c_void_p * max(1, S))()
+    width = np.zeros(max(1, S), dtype=np.int32)
+    for s_, (ids, cnt) in enumerate(idlists):
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        cnt = np.ascontiguousarray(cnt, dtype=np.uint8)
+        keep += [ids, cnt]
+        sid[s_] = ids.ctypes.data
+        scnt[s_] = cnt.ctypes.data
+        width[s_] = ids.shape[1]
+    flat, ioff = [], [0]
+    for cl in id_clauses:
+        flat.extend(cl)
+        ioff.append(len(flat))
+    ic = np.zeros(max(1, len(flat)), dtype=ID_CLAUSE_DTYPE)
+    for i, (slot, rev, ids) in enumerate(flat):
+        arr = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+        keep.append(arr)
+        ic[i]["ids"] = arr.ctypes.data
+        ic[i]["n"] = len(arr)
+        ic[i]["slot"] = slot
+        ic[i]["reverse"] = rev
+    ioff = np.array(ioff, dtype=np.int32)
+    ids_o = np.zeros((B, K), dtype=np.int64)
+    sc = np.zeros((B, K), dtype=np.float64)
+    ps = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_search_idc(dtype, d, n, row0, _p(emb), _p(attrs), attrs.shape[1], _p(live), S,
+                                 ctypes.cast(sid, ctypes.c_void_p), _p(width), ctypes.cast(scnt, ctypes.c_void_p),
+                                 _p(q), B, V, _p(ca), _p(off), _p(ic), _p(ioff), K, _p(ids_o), _p(sc), _p(ps))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return ids_o, sc, ps

@@ -191,6 +191,80 @@ int oracle_search(int dtype, int d, int64_t n, int64_t row0, const void* emb,
   return 0;
 }
 
+// ID-list clauses ("Each query clause could contain multiple attributes. Feasible
+// items should satisfy all clauses, requiring at least one of the attribute in each clauses is
+// matched. Reverse clauses are also supported ... we store all clause attributes in a single
+// matrix ... and have an extra counting matrix to record the number of attributes for each item in
+// each clause"; attributes "converted to 64-bit integers"). Item i's attribute set in slot
+// s = the first counts[s][i] entries of ids[s][i][0..A_s); a clause (slot, reverse, query id list)
+// passes iff (item set INTERSECT query set is non-empty) XOR reverse -- a literal double loop here.
+struct IdClause {       // the oracle's own record: 16 B
+  const uint64_t* ids;
+  int32_t n;
+  uint8_t slot;
+  uint8_t reverse;
+  uint8_t pad[2];
+};
+
+bool id_clause_passes(const uint64_t* const* slot_ids, const int32_t* slot_width, const uint8_t* const* slot_counts,
+                      int64_t i, const IdClause& c) {
+  const int A = slot_width[c.slot];
+  const int cnt = slot_counts[c.slot][i];
+  bool hit = false;
+  for (int a = 0; a < cnt; ++a)
+    for (int q = 0; q < c.n; ++q)
+      if (slot_ids[c.slot][i * A + a] == c.ids[q]) hit = true;
+  return c.reverse ? !hit : hit;
+}
+
+// Filtered top-K with bitmask clauses AND ID-list clauses (same definition as oracle_search plus
+// the ID-list clauses of each query). slot_ids[s]: [n][A_s] u64 row-major, slot_counts[s]: [n].
+int oracle_search_idc(int dtype, int d, int64_t n, int64_t row0, const void* emb, const uint64_t* attrs, int W,
+                      const uint8_t* live, int S, const uint64_t* const* slot_ids, const int32_t* slot_width,
+                      const uint8_t* const* slot_counts, const void* queries, int B, int V, const void* clauses,
+                      const int32_t* clause_off, const void* id_clauses, const int32_t* id_off, int K,
+                      int64_t* out_ids, double* out_scores, int64_t* out_pass) {
+  if (K < 1 || B < 1 || V < 1 || d < 1 || W < 1 || n < 0 || S < 0) return -1;
+  const Clause* cl_all = (const Clause*)clauses;
+  const IdClause* ic_all = (const IdClause*)id_clauses;
+  const int64_t qstride = (int64_t)d * (dtype == O_F32 ? 4 : dtype == O_I8 ? 1 : 2);
+  for (int b = 0; b < B; ++b) {
+    if (clause_off[b + 1] < clause_off[b] || id_off[b + 1] < id_off[b]) return -1;
+    for (int c = clause_off[b]; c < clause_off[b + 1]; ++c)
+      if (cl_all[c].word >= W || cl_all[c].mask == 0) return -1;
+    for (int c = id_off[b]; c < id_off[b + 1]; ++c)
+      if (ic_all[c].slot >= S || ic_all[c].n < 1) return -1;   // an empty ID list is rejected (reading R3)
+  }
+  for (int b = 0; b < B; ++b) {
+    const Clause* cl = cl_all + clause_off[b];
+    const int ncl = clause_off[b + 1] - clause_off[b];
+    std::vector<Cand> C;
+    for (int64_t i = 0; i < n; ++i) {
+      if (!live[i]) continue;
+      if (!item_passes(attrs, W, i, cl, ncl)) continue;
+      bool ok = true;
+      for (int c = id_off[b]; c < id_off[b + 1]; ++c)
+        if (!id_clause_passes(slot_ids, slot_width, slot_counts, i, ic_all[c])) ok = false;
+      if (!ok) continue;
+      double s = -std::numeric_limits<double>::infinity();
+      for (int v = 0; v < V; ++v) {
+        const void* q = (const char*)queries + ((int64_t)b * V + v) * qstride;
+        s = std::max(s, dot(emb, q, dtype, d, i));
+      }
+      if (s == 0.0) s = 0.0;
+      C.push_back({s, row0 + i});
+    }
+    std::sort(C.begin(), C.end(), better);
+    out_pass[b] = (int64_t)C.size();
+    for (int j = 0; j < K; ++j) {
+      const int64_t at = (int64_t)b * K + j;
+      out_ids[at] = j < (int64_t)C.size() ? C[j].id : -1;
+      out_scores[at] = j < (int64_t)C.size() ? C[j].s : -std::numeric_limits<double>::infinity();
+    }
+  }
+  return 0;
+}
+
 // Union of L result lists for the same B queries (one per shard), then top-K by the same order.
 // ids/scores: [L][B][Kin] (-1 padded); pass: [L][B]. Output [B][K], pass summed.
 // Definition used for sharding (reading R13): result on the concatenated index.

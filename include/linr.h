@@ -272,6 +272,54 @@ int linr_search_v3(linr_index* index, const void* queries_dev, int32_t B, int32_
                    double keep, void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev,
                    float* out_scores_dev, int64_t* out_pass_dev, int64_t* out_kept_dev, void* stream);
 
+/* ---------------------------------------------------------------- ID-list clauses
+ * "Each query clause could contain multiple attributes. Feasible items should satisfy all
+ * clauses, requiring at least one of the attribute in each clauses is matched. Reverse clauses
+ * are also supported ... we store all clause attributes in a single matrix ... and have an extra
+ * counting matrix to record the number of attributes for each item in each clause";
+ * attributes are "converted to 64-bit integers before GPU comparison". This is the
+ * high-cardinality companion of the bitmask clauses (geo, company, title as 64-bit ids).
+ * An index may carry up to LINR_MAX_ID_SLOTS slots; slot s holds up to widths[s] ids per item. */
+#define LINR_MAX_ID_SLOTS 4
+#define LINR_MAX_IDS_PER_ITEM 16
+
+/* Query-side clause on an ID-list slot: passes iff (item ids INTERSECT ids_host[0..n)) != {}
+ * XOR reverse. ids_host needs no order (the library sorts and de-duplicates a copy); n >= 1
+ * (an empty list is rejected: omit the clause, reading R3); <= 1024 ids over one query's ID
+ * clauses. */
+typedef struct {
+  const uint64_t* ids_host;
+  int32_t n;
+  uint8_t slot;
+  uint8_t reverse;
+  uint8_t pad[2];
+} linr_id_clause;
+
+/* Caller-owned device storage for `slots` ID-list slots of widths[s] ids per item (all rows). */
+size_t linr_idlists_storage_bytes(const linr_index* index, int32_t slots, const int32_t* widths_host);
+
+/* Attach ID-list slots (setup call: zero-fills the counts synchronously; no row has ids yet). */
+int linr_idlists_attach(linr_index* index, int32_t slots, const int32_t* widths_host, void* storage_dev);
+
+/* Write the ID lists of slot `slot` for n rows: rows_dev = global ids (live upsert; out-of-shard
+ * ids skipped and counted), or NULL for the contiguous rows [row0, row0+n) (bulk load).
+ * ids_dev [n][widths[slot]] u64 (entries past the row's count are ignored), counts_dev [n] u8
+ * (<= width). Stream-ordered like linr_index_update_rows. */
+int linr_idlists_set_rows(linr_index* index, int32_t slot, const int64_t* rows_dev, int64_t row0, int64_t n,
+                          const uint64_t* ids_dev, const uint8_t* counts_dev, void* stream);
+
+/* linr_search with ID-list clauses in addition to the bitmask clauses (CSR by
+ * id_clause_off_host[B+1]). The ID clauses of each query are evaluated by a filter kernel into a
+ * per-query liveness bitmap (live AND every ID clause); the fused scan then runs one user per
+ * launch on that bitmap with the bitmask clauses. Same outputs as linr_search. Workspace:
+ * linr_search_idc_workspace_bytes. */
+size_t linr_search_idc_workspace_bytes(const linr_index* index, int32_t B, int32_t V, int32_t K);
+int linr_search_idc(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
+                    const linr_clause* clauses_host, const int32_t* clause_off_host,
+                    const linr_id_clause* id_clauses_host, const int32_t* id_clause_off_host, int32_t K,
+                    void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, float* out_scores_dev,
+                    int64_t* out_pass_dev, void* stream);
+
 /* Device-side synthetic data generator (benchmark plumbing, not part of the method): fills local
  * rows [row_begin, row_begin+n) of the index with the counter-based recipe of DESIGN.md
  * "Input recipe" (identical bytes to datagen/ in Python), marks them live and raises the

@@ -109,6 +109,12 @@ struct linr_index {
   int code_k = 0, code_L = 0;
   int32_t* c_src = nullptr;
   int8_t* c_sign = nullptr;
+  // ID-list attribute slots (linr_idlists_attach): ids [sumA][cap_pad] u64, counts [S][cap_pad] u8
+  uint64_t* idl_ids = nullptr;
+  uint8_t* idl_cnt = nullptr;
+  int idl_S = 0;
+  int idl_A[4] = {0, 0, 0, 0};
+  int idl_off[4] = {0, 0, 0, 0};
   void* comm = nullptr;         // NCCL communicator over the shards (linr_comm_init)
   int comm_rank = 0, comm_world = 1;
   bool prof = false;
@@ -164,9 +170,10 @@ struct Plan {
 
 constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) (static_assert in scan_gemv.cuh)
 
-bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why) {
+bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why, bool one_user = false) {
   const int dt = ix->d.dtype, dim = ix->d.dim;
   int nu = std::max(1, std::min(B, std::min(kMaxUsers, 8 / V)));
+  if (one_user) nu = 1;   // per-user liveness bitmaps (ID-list clauses): one user per launch
   // The ring scan runs one user per launch: a user's key buffer then gets most of the shared
   // memory the ring leaves (measured at c2 HIGH, B = 4 / 8: one launch per user 0.31 / 0.62 ms,
   // users sharing a launch -- and its buffers, hence many compactions -- 0.81 / 2.48 ms).
@@ -174,7 +181,7 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
   const int nu_first = nu;
   if (ws_ok) nu = 1;
   if (const char* mn = std::getenv("LINR_MAX_NU")) nu = std::max(1, std::min(nu, std::atoi(mn)));
-  for (int pass = ws_ok ? 0 : 1; pass < 2; ++pass, nu = nu_first) {
+  for (int pass = ws_ok ? 0 : 1; pass < 2; ++pass, nu = one_user ? 1 : nu_first) {
   for (; nu >= 1; --nu) {
     const int nqv = next_pow2(nu * V);
     if (nqv > 8 || !scan_gemv_supported(dt, dim, nqv)) continue;
@@ -301,7 +308,7 @@ bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* 
 
 int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
                 void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
-                int64_t* out_pass, cudaStream_t st);
+                int64_t* out_pass, cudaStream_t st, const uint32_t* live_ovr = nullptr, size_t live_ovr_words = 0);
 
 // Clause table [B][16] KClause followed by counts [B] int, copied host -> pinned slot -> dst_dev on
 // st (one copy). The pinned slot is reused kPinSlots calls later, once its copy has executed.
@@ -485,18 +492,20 @@ int validate_query(const linr_index* ix, const void* q, int B, int V, const linr
 }
 
 // scan (+ per-CTA lists) then merge into either ids/scores (mode 0) or keys (mode 1)
+// live_ovr: per-user liveness bitmaps [B][live_ovr_words] replacing the index's (ID-list clauses
+// already applied, see linr_search_idc); forces the GEMV path with one user per launch.
 int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
                 void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
-                int64_t* out_pass, cudaStream_t st) {
+                int64_t* out_pass, cudaStream_t st, const uint32_t* live_ovr, size_t live_ovr_words) {
   std::string why;
   int rc = validate_query(ix, q, B, V, cl, off, K, &why);
   if (rc != LINR_OK) return fail(rc, why);
   if (mode == 0 && (!out_ids || !out_scores)) return fail(LINR_EINVAL, "null outputs");
   if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
-  if (use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) && !ix->force_gemv)
+  if (!live_ovr && use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) && !ix->force_gemv)
     return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
   Plan pl;
-  if (!make_plan(ix, B, V, K, &pl, &why)) return fail(LINR_EUNSUPPORTED, why);
+  if (!make_plan(ix, B, V, K, &pl, &why, live_ovr != nullptr)) return fail(LINR_EUNSUPPORTED, why);
   const WsLayout wl = ws_layout(pl, B, K);
   if (!ws || ws_bytes < wl.end) return fail(LINR_ENOMEM, "workspace too small");
   DeviceGuard dg(ix->d.device);
@@ -557,7 +566,7 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
     std::memset(&p, 0, sizeof(p));
     p.emb = ix->emb;
     p.attr = ix->attr;
-    p.live = ix->live;
+    p.live = live_ovr ? live_ovr + (size_t)u0 * live_ovr_words : ix->live;
     p.hdr = ix->hdr;
     p.cap_pad = ix->cap_pad;
     p.row0 = (uint32_t)ix->d.global_row0;
@@ -1335,6 +1344,166 @@ int linr_search_v3(linr_index* ix, const void* q, int32_t B, int32_t V, const li
   if (!(keep > 0.0)) return fail(LINR_EINVAL, "keep must be in (0, 1]");
   return code_pipeline(ix, q, B, V, cl, off, K, keep, ws, ws_bytes, out_ids, nullptr, out_scores, out_pass, out_kept,
                        (cudaStream_t)stream);
+}
+
+
+// ------------------------------------------------------------------ ID-list clauses (idlist.cu)
+static bool idl_desc_ok(int32_t slots, const int32_t* widths, std::string* why) {
+  if (slots < 1 || slots > LINR_MAX_ID_SLOTS || !widths) { *why = "slots must be in [1, 4]"; return false; }
+  for (int s = 0; s < slots; ++s)
+    if (widths[s] < 1 || widths[s] > LINR_MAX_IDS_PER_ITEM) { *why = "width must be in [1, 16]"; return false; }
+  return true;
+}
+
+size_t linr_idlists_storage_bytes(const linr_index* ix, int32_t slots, const int32_t* widths) {
+  std::string why;
+  if (!ix || !idl_desc_ok(slots, widths, &why)) return 0;
+  size_t A = 0;
+  for (int s = 0; s < slots; ++s) A += widths[s];
+  return align256(A * ix->cap_pad * 8) + align256((size_t)slots * ix->cap_pad);
+}
+
+int linr_idlists_attach(linr_index* ix, int32_t slots, const int32_t* widths, void* storage) {
+  std::string why;
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (!idl_desc_ok(slots, widths, &why)) return fail(LINR_EINVAL, why);
+  if (!storage) return fail(LINR_EINVAL, "null storage");
+  if (ix->idl_ids) return fail(LINR_EINVAL, "ID lists already attached");
+  DeviceGuard dg(ix->d.device);
+  size_t A = 0;
+  for (int s = 0; s < slots; ++s) {
+    ix->idl_A[s] = widths[s];
+    ix->idl_off[s] = (int)A;
+    A += widths[s];
+  }
+  ix->idl_S = slots;
+  ix->idl_ids = (uint64_t*)storage;
+  ix->idl_cnt = (uint8_t*)((char*)storage + align256(A * ix->cap_pad * 8));
+  cudaError_t e = cudaMemset(ix->idl_cnt, 0, (size_t)slots * ix->cap_pad);   // setup: no row has ids yet
+  if (e != cudaSuccess) return cuda_fail(e, "ID-list init");
+  return LINR_OK;
+}
+
+int linr_idlists_set_rows(linr_index* ix, int32_t slot, const int64_t* rows, int64_t row0, int64_t n,
+                          const uint64_t* ids, const uint8_t* counts, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (!ix->idl_ids) return fail(LINR_EINVAL, "no ID lists attached");
+  if (slot < 0 || slot >= ix->idl_S) return fail(LINR_EINVAL, "bad slot");
+  if (n < 0) return fail(LINR_EINVAL, "n < 0");
+  if (n == 0) return LINR_OK;
+  if (!ids || !counts) return fail(LINR_EINVAL, "null input");
+  const int64_t r0 = row0 - ix->d.global_row0;
+  if (!rows && (r0 < 0 || r0 + n > ix->d.capacity_rows)) return fail(LINR_ERANGE, "rows outside this shard");
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = launch_idl_set_rows(rows, r0, ix->d.global_row0, ix->d.capacity_rows, n, ix->idl_A[slot], ids, counts,
+                                      ix->idl_ids + (size_t)ix->idl_off[slot] * ix->cap_pad,
+                                      ix->idl_cnt + (size_t)slot * ix->cap_pad, ix->cap_pad, ix->hdr,
+                                      (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ID-list set rows");
+  return LINR_OK;
+}
+
+namespace {
+struct IdcWs {
+  size_t bitmaps, qcl, qncl, qids, local, end;
+};
+IdcWs idc_layout(const linr_index* ix, int B, int V, int K) {
+  IdcWs w;
+  w.bitmaps = 0;
+  w.qcl = align256((size_t)B * (ix->cap_pad / 8));
+  w.qncl = w.qcl + align256((size_t)B * 16 * 16);
+  w.qids = w.qncl + align256((size_t)B * 4);
+  w.local = w.qids + align256((size_t)B * kIdlMaxQueryIds * 8);
+  Plan pl;
+  std::string why;
+  size_t loc = 0;
+  if (make_plan(ix, B, V, K, &pl, &why, true)) loc = ws_layout(pl, B, K).end;
+  w.end = loc ? w.local + loc : 0;
+  return w;
+}
+}  // namespace
+
+size_t linr_search_idc_workspace_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t K) {
+  if (!ix || B < 1 || V < 1 || V > LINR_MAX_V || K < 1 || K > LINR_MAX_K) return 0;
+  return idc_layout(ix, B, V, K).end;
+}
+
+int linr_search_idc(linr_index* ix, const void* q, int32_t B, int32_t V, const linr_clause* cl, const int32_t* off,
+                    const linr_id_clause* icl, const int32_t* ioff, int32_t K, void* ws, size_t ws_bytes,
+                    int64_t* out_ids, float* out_scores, int64_t* out_pass, void* stream) {
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (!ioff) return fail(LINR_EINVAL, "null ID clause offsets");
+  if (!ix->idl_ids) return fail(LINR_EINVAL, "no ID lists attached (linr_idlists_attach)");
+  if (B < 1 || V < 1 || V > LINR_MAX_V || K < 1 || K > LINR_MAX_K) return fail(LINR_EINVAL, "bad B/V/K");
+  if (ioff[0] != 0) return fail(LINR_EINVAL, "id_clause_off[0] must be 0");
+  // host validation + staging: per query its ID clauses (slot, reverse, first id, count) and the
+  // sorted, de-duplicated id lists (the filter kernel binary-searches them)
+  std::vector<int32_t> hcl((size_t)B * 16 * 4, 0), hncl(B, 0);
+  std::vector<uint64_t> hids;
+  for (int b = 0; b < B; ++b) {
+    const int n = ioff[b + 1] - ioff[b];
+    if (n < 0) return fail(LINR_EINVAL, "ID clause offsets must be non-decreasing");
+    if (n > LINR_MAX_CLAUSES) return fail(LINR_EINVAL, "more than 16 ID clauses in one query");
+    if (n > 0 && !icl) return fail(LINR_EINVAL, "null ID clauses");
+    size_t qtot = 0;
+    for (int c = 0; c < n; ++c) {
+      const linr_id_clause& k = icl[ioff[b] + c];
+      if (k.slot >= ix->idl_S) return fail(LINR_EINVAL, "ID clause slot >= attached slots");
+      if (k.n < 1 || !k.ids_host) return fail(LINR_EINVAL, "empty ID clause (omit the clause instead)");
+      if (k.reverse > 1) return fail(LINR_EINVAL, "ID clause reverse must be 0 or 1");
+      std::vector<uint64_t> v(k.ids_host, k.ids_host + k.n);
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      qtot += v.size();
+      if (qtot > (size_t)kIdlMaxQueryIds) return fail(LINR_EINVAL, "more than 1024 query ids in one query");
+      int32_t* r = &hcl[((size_t)b * 16 + c) * 4];
+      r[0] = k.slot;
+      r[1] = k.reverse;
+      r[2] = (int32_t)hids.size();
+      r[3] = (int32_t)v.size();
+      hids.insert(hids.end(), v.begin(), v.end());
+    }
+    hncl[b] = n;
+  }
+  const IdcWs w = idc_layout(ix, B, V, K);
+  if (w.end == 0) return fail(LINR_EUNSUPPORTED, "no scan configuration for this shape");
+  if (!ws || ws_bytes < w.end) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  // the staging copies go through a pinned slot (the caller's host arrays may be freed on return)
+  linr_index::PinSlot& ps = ix->pin[ix->pin_next];
+  ix->pin_next = (ix->pin_next + 1) % kPinSlots;
+  if (!ps.ev && cudaEventCreateWithFlags(&ps.ev, cudaEventDisableTiming) != cudaSuccess)
+    return fail(LINR_ECUDA, "staging event");
+  cudaEventSynchronize(ps.ev);
+  const size_t b1 = hcl.size() * 4, b2 = hncl.size() * 4, b3 = std::max<size_t>(8, hids.size() * 8);
+  const size_t need = align256(b1) + align256(b2) + align256(b3);
+  if (ps.bytes < need) {
+    if (ps.p) cudaFreeHost(ps.p);
+    ps.p = nullptr;
+    ps.bytes = 0;
+    if (cudaHostAlloc(&ps.p, need, cudaHostAllocDefault) != cudaSuccess) return fail(LINR_ENOMEM, "pinned staging");
+    ps.bytes = need;
+  }
+  char* h = (char*)ps.p;
+  std::memcpy(h, hcl.data(), b1);
+  std::memcpy(h + align256(b1), hncl.data(), b2);
+  if (!hids.empty()) std::memcpy(h + align256(b1) + align256(b2), hids.data(), hids.size() * 8);
+  cudaError_t e = cudaMemcpyAsync(W + w.qcl, h, b1, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(W + w.qncl, h + align256(b1), b2, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !hids.empty())
+    e = cudaMemcpyAsync(W + w.qids, h + align256(b1) + align256(b2), hids.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(ps.ev, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ID clause staging");
+  const int64_t words = ix->cap_pad / 32;
+  const int grid_x = (int)std::min<int64_t>(ix->cap_pad / 256, (int64_t)ix->num_sms * 8);
+  e = launch_idl_filter(ix->idl_ids, ix->idl_cnt, ix->cap_pad, ix->live, ix->hdr, ix->idl_off, (const int*)(W + w.qncl),
+                        W + w.qcl, (const uint64_t*)(W + w.qids), B, (uint32_t*)(W + w.bitmaps), grid_x, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ID-list filter launch");
+  if (ix->prof) ix->prof_launches += 1;
+  return search_impl(ix, q, B, V, cl, off, K, W + w.local, ws_bytes - w.local, 0, out_ids, out_scores, nullptr,
+                     out_pass, st, (const uint32_t*)(W + w.bitmaps), (size_t)words);
 }
 
 }  // extern "C"

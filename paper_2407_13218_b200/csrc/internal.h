@@ -251,6 +251,15 @@ cudaError_t launch_code_pad(const int64_t* kept, int nu, int64_t K, int64_t* out
                             cudaStream_t st);
 cudaError_t launch_rerank(int dtype, const RerankParams& p, int grid, cudaStream_t st);
 
+// ---------------------------------------------------------------- ID-list clauses (idlist.cu)
+constexpr int kIdlMaxQueryIds = 1024;   // query ids over all ID clauses of one query
+cudaError_t launch_idl_filter(const uint64_t* ids, const uint8_t* counts, int64_t cap_pad, const uint32_t* live,
+                              const DevHeader* hdr, const int* slot_off, const int* q_ncl, const void* q_cl,
+                              const uint64_t* q_ids, int B, uint32_t* out, int grid_x, cudaStream_t st);
+cudaError_t launch_idl_set_rows(const int64_t* rows, int64_t r0, int64_t grow0, int64_t cap, int64_t n, int A,
+                                const uint64_t* src_ids, const uint8_t* src_cnt, uint64_t* dst_ids, uint8_t* dst_cnt,
+                                int64_t cap_pad, DevHeader* hdr, cudaStream_t st);
+
 // NCCL communicator of a row-sharded index (comm.cu; NCCL loaded at run time)
 int comm_create(int device, const uint8_t id[128], int rank, int world, void** out);
 void comm_destroy(void* comm);

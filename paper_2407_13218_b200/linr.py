@@ -26,7 +26,8 @@ ABI_FUNCTIONS = (
     "linr_generate_rows", "linr_index_profile", "linr_index_profile_read", "linr_debug_timers", "linr_debug_read",
     "linr_last_error", "linr_version", "linr_index_counters", "linr_nccl_unique_id", "linr_comm_init",
     "linr_codes_storage_bytes", "linr_codes_attach", "linr_oporp_encode", "linr_code_search_workspace_bytes",
-    "linr_code_search", "linr_search_v3",
+    "linr_code_search", "linr_search_v3", "linr_idlists_storage_bytes", "linr_idlists_attach",
+    "linr_idlists_set_rows", "linr_search_idc_workspace_bytes", "linr_search_idc",
 )
 
 
@@ -44,6 +45,34 @@ class _Counters(ctypes.Structure):
 class _Oporp(ctypes.Structure):
     _fields_ = [("bits", ctypes.c_int32), ("L", ctypes.c_int32), ("src_host", ctypes.c_void_p),
                 ("sign_host", ctypes.c_void_p)]
+
+
+class _IdClause(ctypes.Structure):
+    _fields_ = [("ids_host", ctypes.c_void_p), ("n", ctypes.c_int32), ("slot", ctypes.c_uint8),
+                ("reverse", ctypes.c_uint8), ("pad", ctypes.c_uint8 * 2)]
+
+
+class IdClauses:
+    """Per-query ID-list clauses [(slot, reverse, ids), ...] in the ABI's CSR layout (host memory)."""
+
+    def __init__(self, id_clauses):
+        flat, off = [], [0]
+        for cl in id_clauses:
+            flat.extend(cl)
+            off.append(len(flat))
+        self.keep = []
+        self.arr = (_IdClause * max(1, len(flat)))()
+        for i, (slot, rev, ids) in enumerate(flat):
+            a = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+            self.keep.append(a)
+            self.arr[i].ids_host = a.ctypes.data
+            self.arr[i].n = len(a)
+            self.arr[i].slot = int(slot)
+            self.arr[i].reverse = int(rev)
+        self.off = np.array(off, dtype=np.int32)
+        self.B = len(id_clauses)
+        self.p_arr = ctypes.addressof(self.arr)
+        self.p_off = self.off.ctypes.data
 
 
 class _Desc(ctypes.Structure):
@@ -78,6 +107,11 @@ def library():
         "linr_index_counters": ([P, ctypes.POINTER(_Counters), P], ctypes.c_int),
         "linr_nccl_unique_id": ([P], ctypes.c_int),
         "linr_codes_storage_bytes": ([P, ctypes.POINTER(_Oporp)], SZ),
+        "linr_idlists_storage_bytes": ([P, I32, P], SZ),
+        "linr_idlists_attach": ([P, I32, P, P], ctypes.c_int),
+        "linr_idlists_set_rows": ([P, I32, P, I64, I64, P, P, P], ctypes.c_int),
+        "linr_search_idc_workspace_bytes": ([P, I32, I32, I32], SZ),
+        "linr_search_idc": ([P, P, I32, I32, P, P, P, P, I32, P, SZ, P, P, P, P], ctypes.c_int),
         "linr_codes_attach": ([P, ctypes.POINTER(_Oporp), P, P], ctypes.c_int),
         "linr_oporp_encode": ([P, P, I64, P, P], ctypes.c_int),
         "linr_code_search_workspace_bytes": ([P, I32, I32, I64, I32], SZ),
@@ -194,6 +228,60 @@ class Index:
         _check(library().linr_comm_init(self._h, ctypes.addressof(buf), rank, world))
         self._ws = {}   # workspaces grow by the exchange buffers
         self.comm_world = world
+
+    # ------------------------------------------------------------ ID-list clauses
+    def attach_idlists(self, widths):
+        """Attach ID-list slots with widths[s] 64-bit ids per item (linr_idlists_attach)."""
+        w = np.ascontiguousarray(np.asarray(widths, dtype=np.int32))
+        L = library()
+        n = L.linr_idlists_storage_bytes(self._h, len(w), w.ctypes.data)
+        if n == 0:
+            raise LinrError(-1, "invalid ID-list slot widths")
+        self.idl_storage = torch.empty(n, dtype=torch.uint8, device=self.device)
+        _check(L.linr_idlists_attach(self._h, len(w), w.ctypes.data, self.idl_storage.data_ptr()))
+        self.idl_widths = w.tolist()
+
+    def set_idlists(self, slot: int, ids: torch.Tensor, counts: torch.Tensor, rows: torch.Tensor | None = None,
+                    row0: int | None = None):
+        """Write slot `slot`'s id lists: ids [n][width] (int64 view of u64), counts [n] uint8, for
+        global rows `rows` (upsert) or the contiguous rows from row0 (load)."""
+        ids = _as_i64(ids).contiguous()
+        counts = counts.to(torch.uint8).contiguous()
+        n = ids.shape[0]
+        assert ids.device == self.device and counts.device == self.device
+        assert ids.shape[1] == self.idl_widths[slot] and counts.numel() == n
+        rp = None
+        if rows is not None:
+            rows = rows.to(torch.int64).contiguous()
+            assert rows.device == self.device and rows.numel() == n
+            rp = rows.data_ptr()
+        r0 = self.row0 if row0 is None else row0
+        _check(library().linr_idlists_set_rows(self._h, slot, rp, r0, n, ids.data_ptr(), counts.data_ptr(),
+                                               _stream(self.device)))
+
+    def search_idc(self, queries: torch.Tensor, clauses, id_clauses, K: int):
+        """Filtered top-K with bitmask clauses and ID-list clauses (linr_search_idc)."""
+        q = self._q(queries)
+        B, V, _ = q.shape
+        cl = clause_array(clauses)
+        ic = id_clauses if isinstance(id_clauses, IdClauses) else IdClauses(id_clauses)
+        assert cl.B == B and ic.B == B
+        ids = torch.empty((B, K), dtype=torch.int64, device=self.device)
+        sc = torch.empty((B, K), dtype=torch.float32, device=self.device)
+        ps = torch.empty(B, dtype=torch.int64, device=self.device)
+        L = library()
+        n = L.linr_search_idc_workspace_bytes(self._h, B, V, K)
+        if n == 0:
+            raise LinrError(-1, f"no ID-clause workspace for B={B} V={V} K={K}")
+        key = ("idc", B, V, K)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < n:
+            ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        _check(L.linr_search_idc(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, ic.p_arr, ic.p_off, K,
+                                 ws.data_ptr(), ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
+                                 _stream(self.device)))
+        return ids, sc, ps
 
     # ------------------------------------------------------------ quantised path (PAPER.md §3.2)
     def attach_codes(self, bits: int, src, sign):

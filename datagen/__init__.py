@@ -28,6 +28,8 @@ UPDATE_SEED = 0x4429
 # counter streams
 S_CLUSTER, S_CENTER, S_NOISE, S_ATTR, S_QROW, S_QNOISE, S_QCLAUSE, S_OPORP = 1, 2, 3, 4, 5, 6, 7, 8
 S_IDL, S_IDVAL, S_QIDL = 9, 10, 11
+S_SCORER = 12
+SCORER_SEED = 0x4318   # PAPER.md P:4318 (Hadamard MLP)
 ID_SENTINEL = np.uint64(0xFFFFFFFFFFFFFFFF)   # padding of ID-list rows
 OPORP_SEED = 0x4294   # PAPER.md P:4294 (Sign-OPORP)
 
@@ -384,3 +386,33 @@ def gen_id_clauses(qseed: int, dseed: int, B: int, slot: int, A: int, universe: 
         ids = vals if raw else id_of(dseed, vals)
         out.append([(slot, reverse, np.unique(ids))])
     return out
+
+
+# ---------------------------------------------------------------- learned-scorer weights (synthetic)
+def _uniform_weights(seed: int, tag: int, shape, scale: float) -> np.ndarray:
+    """float32 weights uniform in [-scale, scale), multiples of scale * 2^-11 (counter-based)."""
+    n = int(np.prod(shape))
+    h = h2(seed, S_SCORER, U64(tag), np.arange(n, dtype=U64))
+    u = ((h >> U64(53)).astype(np.int64) - 1024).astype(np.float32) * np.float32(scale / 1024.0)
+    return u.reshape(shape)
+
+
+def scorer_weights(seed: int, kind: str, d: int, F: int = 50, H: int = 10, K: int = 4, dc: int = 32, G: int = 16):
+    """Synthetic weights of a learned scorer (§3.3; training is out of scope):
+    'hadamard' -- member/item MLP width F (Table 1: [50]), head [H, 1] (Table 1: [10, 1]);
+    'mol'      -- K components of width dc (user/item projections), gate hidden width G.
+    Fan-in-scaled uniform values so scores stay O(1)."""
+    s_in = 1.0 / np.sqrt(d)
+    if kind == "hadamard":
+        return {"kind": 1, "F": F, "H": H,
+                "Wm": _uniform_weights(seed, 1, (F, d), s_in), "bm": _uniform_weights(seed, 2, (F,), 0.1),
+                "Wi": _uniform_weights(seed, 3, (F, d), s_in), "bi": _uniform_weights(seed, 4, (F,), 0.1),
+                "W1": _uniform_weights(seed, 5, (H, F), 1.0 / np.sqrt(F)), "b1": _uniform_weights(seed, 6, (H,), 0.1),
+                "w2": _uniform_weights(seed, 7, (H,), 1.0 / np.sqrt(H)), "b2": _uniform_weights(seed, 8, (1,), 0.1)}
+    if kind == "mol":
+        return {"kind": 2, "K": K, "dc": dc, "G": G,
+                "Fk": _uniform_weights(seed, 11, (K * dc, d), s_in), "Gk": _uniform_weights(seed, 12, (K * dc, d), s_in),
+                "Wgu": _uniform_weights(seed, 13, (G, d), s_in), "Wgx": _uniform_weights(seed, 14, (G, d), s_in),
+                "bg": _uniform_weights(seed, 15, (G,), 0.1), "Wo": _uniform_weights(seed, 16, (K, G), 1.0 / np.sqrt(G)),
+                "bo": _uniform_weights(seed, 17, (K,), 0.1)}
+    raise ValueError(kind)

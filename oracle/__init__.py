@@ -21,7 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "linr_oracle.cpp")
-_SRCS = [_SRC, os.path.join(_HERE, "oporp_oracle.cpp")]
+_SRCS = [_SRC, os.path.join(_HERE, "oporp_oracle.cpp"), os.path.join(_HERE, "scorer_oracle.cpp")]
 _LIB = os.path.join(_HERE, "liblinr_oracle.so")
 _lib = None
 
@@ -70,6 +70,10 @@ def lib():
         L.oracle_search_v3.restype = I
         L.oracle_search_idc.argtypes = [I, I, I64, I64, P, P, I, P, I, P, P, P, P, I, I, P, P, P, P, I, P, P, P]
         L.oracle_search_idc.restype = I
+        L.oracle_scorer_score.argtypes = [P, I, I, P, I64, P, I64]
+        L.oracle_scorer_score.restype = ctypes.c_double
+        L.oracle_search_scored.argtypes = [P, I, I, I64, I64, P, P, I, P, P, I, P, P, I, P, P, P]
+        L.oracle_search_scored.restype = I
         _lib = L
     return _lib
 
@@ -292,3 +296,57 @@ def search_idc(dtype, emb, attrs, live, idlists, queries, clauses, id_clauses, K
     if rc != 0:
         raise ValueError("oracle precondition violated")
     return ids_o, sc, ps
+
+
+# ---------------------------------------------------------------- learned scorers (scorer_oracle.cpp)
+class _Scorer(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("F", ctypes.c_int32), ("H", ctypes.c_int32), ("K", ctypes.c_int32),
+                ("dc", ctypes.c_int32), ("G", ctypes.c_int32)] + \
+               [(nm, ctypes.c_void_p) for nm in ("Wm", "bm", "Wi", "bi", "W1", "b1", "w2", "b2", "Fk", "Gk",
+                                                 "Wgu", "Wgx", "bg", "Wo", "bo")]
+
+
+def _scorer(w):
+    """w: dict from datagen.scorer_weights (float32 arrays). Returns (struct, keep-alive list)."""
+    st = _Scorer()
+    st.kind = w["kind"]
+    for k in ("F", "H", "K", "dc", "G"):
+        setattr(st, k, int(w.get(k, 0)))
+    keep = []
+    for nm, _ in _Scorer._fields_[6:]:
+        if nm in w:
+            a = np.ascontiguousarray(w[nm], dtype=np.float32)
+            keep.append(a)
+            setattr(st, nm, a.ctypes.data)
+    return st, keep
+
+
+def scorer_scores(w, dtype, emb, q):
+    """Scores of every row of emb for one query vector q under the learned scorer w."""
+    st, keep = _scorer(w)
+    emb = np.ascontiguousarray(emb)
+    q = np.ascontiguousarray(q).reshape(1, -1)
+    n, d = emb.shape
+    return np.array([lib().oracle_scorer_score(ctypes.byref(st), dtype, d, _p(q), 0, _p(emb), i) for i in range(n)])
+
+
+def search_scored(w, dtype, emb, attrs, live, queries, clauses, K, row0=0):
+    """Filtered top-K under a learned scorer (queries [B][d]). Returns ids, scores (fp64), pass."""
+    st, keep = _scorer(w)
+    emb = np.ascontiguousarray(emb)
+    attrs = np.ascontiguousarray(attrs, dtype=np.uint64)
+    n, d = emb.shape
+    live = np.ascontiguousarray(live, dtype=np.uint8)
+    q = np.ascontiguousarray(queries).reshape(-1, d)
+    B = q.shape[0]
+    ca, off = csr(clauses)
+    if len(ca) == 0:
+        ca = np.zeros(1, dtype=CLAUSE_DTYPE)
+    ids = np.zeros((B, K), dtype=np.int64)
+    sc = np.zeros((B, K), dtype=np.float64)
+    ps = np.zeros(B, dtype=np.int64)
+    rc = lib().oracle_search_scored(ctypes.byref(st), dtype, d, n, row0, _p(emb), _p(attrs), attrs.shape[1],
+                                    _p(live), _p(q), B, _p(ca), _p(off), K, _p(ids), _p(sc), _p(ps))
+    if rc != 0:
+        raise ValueError("oracle precondition violated")
+    return ids, sc, ps

@@ -320,6 +320,40 @@ int linr_search_idc(linr_index* index, const void* queries_dev, int32_t B, int32
                     void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, float* out_scores_dev,
                     int64_t* out_pass_dev, void* stream);
 
+/* ---------------------------------------------------------------- learned scorers (§3.3)
+ * The filtered exhaustive search with a learned similarity in place of the dot product, weights
+ * supplied by the caller (float32 host arrays, row-major; training is out of scope):
+ *  Hadamard MLP (Table 1 "Member & Item MLP [50]+[10, 1]"):
+ *     s(q, x) = w2 . ReLU(W1 ((Wm q + bm) (.) (Wi x + bi)) + b1) + b2
+ *     Wm, Wi [F][dim]; bm, bi [F]; W1 [H][F]; b1, w2 [H]; b2 [1]
+ *  Mixture-of-Logits ("phi_MoL(x, u) = sum_k pi_k(x, u) delta_k(x, u)"):
+ *     delta_k = <Fk_k u, Gk_k x> (component k = rows [k*dc, (k+1)*dc) of Fk, Gk [K*dc][dim]),
+ *     pi = softmax(Wo ReLU(Wgu u + Wgx x + bg) + bo); Wgu, Wgx [G][dim]; bg [G]; Wo [K][G]; bo [K]
+ * The query-independent item side (Wi x + bi; or [Gk x, Wgx x]) is computed once per row at
+ * attach time and again whenever rows are loaded, upserted or generated (same stream), so a
+ * search evaluates only the per-query remainder on the passing rows. fp32 arithmetic. */
+#define LINR_SCORER_HADAMARD 1
+#define LINR_SCORER_MOL 2
+typedef struct {
+  int32_t kind;              /* LINR_SCORER_HADAMARD or LINR_SCORER_MOL                */
+  int32_t F, H;              /* Hadamard: member/item width (<= 256), head hidden (<= 64) */
+  int32_t K, dc, G;          /* MoL: components (<= 8), component width (multiple of 4), gate hidden (<= 64) */
+  const float *Wm, *bm, *Wi, *bi, *W1, *b1, *w2, *b2;
+  const float *Fk, *Gk, *Wgu, *Wgx, *bg, *Wo, *bo;
+} linr_scorer;
+
+/* Caller-owned device storage for the scorer weights + the item features of every row. */
+size_t linr_scorer_storage_bytes(const linr_index* index, const linr_scorer* scorer);
+/* Attach a learned scorer (setup call: synchronises `stream`, copies the weights, enqueues the
+ * item features of the rows below the high-water mark). EINVAL on bad widths / null weights. */
+int linr_scorer_attach(linr_index* index, const linr_scorer* scorer, void* storage_dev, void* stream);
+/* Filtered top-K under the attached scorer: queries_dev [B][dim] (one vector per query), clauses
+ * as linr_search, K in [1, 2048]; outputs as linr_search (scores fp32, order score desc / id asc). */
+size_t linr_search_scored_workspace_bytes(const linr_index* index, int32_t B, int32_t K);
+int linr_search_scored(linr_index* index, const void* queries_dev, int32_t B, const linr_clause* clauses_host,
+                       const int32_t* clause_off_host, int32_t K, void* ws_dev, size_t ws_bytes,
+                       int64_t* out_ids_dev, float* out_scores_dev, int64_t* out_pass_dev, void* stream);
+
 /* Device-side synthetic data generator (benchmark plumbing, not part of the method): fills local
  * rows [row_begin, row_begin+n) of the index with the counter-based recipe of DESIGN.md
  * "Input recipe" (identical bytes to datagen/ in Python), marks them live and raises the

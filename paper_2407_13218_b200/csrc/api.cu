@@ -115,6 +115,10 @@ struct linr_index {
   int idl_S = 0;
   int idl_A[4] = {0, 0, 0, 0};
   int idl_off[4] = {0, 0, 0, 0};
+  // learned scorer (linr_scorer_attach): weights + item features y [cap_pad][Fp]
+  bool scorer = false;
+  ScorerDev sw;
+  float* sy = nullptr;
   void* comm = nullptr;         // NCCL communicator over the shards (linr_comm_init)
   int comm_rank = 0, comm_world = 1;
   bool prof = false;
@@ -766,6 +770,11 @@ int linr_index_load(linr_index* ix, int64_t row0, int64_t n, const void* emb, co
                             ix->code_L, ix->c_src, ix->c_sign, ix->codes, st);
     if (e != cudaSuccess) return cuda_fail(e, "load encode");
   }
+  if (ix->scorer) {   // learned-scorer item features follow the rows
+    e = launch_features(ix->d.dtype, ix->emb, ix->d.dim, n, r0, nullptr, 0, ix->d.capacity_rows, ix->sw.M, ix->sw.Mb,
+                        ix->sw.Fm, ix->sw.Fp, ix->sy, st);
+    if (e != cudaSuccess) return cuda_fail(e, "load features");
+  }
   return LINR_OK;
 }
 
@@ -784,6 +793,11 @@ int linr_index_update_rows(linr_index* ix, const int64_t* rows, int64_t n, const
     e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, n, 0, rows, ix->d.global_row0, ix->d.capacity_rows,
                             ix->code_k, ix->code_L, ix->c_src, ix->c_sign, ix->codes, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "update encode");
+  }
+  if (ix->scorer) {
+    e = launch_features(ix->d.dtype, ix->emb, ix->d.dim, n, 0, rows, ix->d.global_row0, ix->d.capacity_rows, ix->sw.M,
+                        ix->sw.Mb, ix->sw.Fm, ix->sw.Fp, ix->sy, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "update features");
   }
   return LINR_OK;
 }
@@ -1040,6 +1054,11 @@ int linr_index_generate(linr_index* ix, uint64_t seed, int32_t mode, int64_t row
     e = launch_oporp_encode(ix->d.dtype, ix->emb, ix->d.dim, n, row_begin, nullptr, 0, ix->d.capacity_rows,
                             ix->code_k, ix->code_L, ix->c_src, ix->c_sign, ix->codes, st);
     if (e != cudaSuccess) return cuda_fail(e, "generate encode");
+  }
+  if (ix->scorer) {
+    e = launch_features(ix->d.dtype, ix->emb, ix->d.dim, n, row_begin, nullptr, 0, ix->d.capacity_rows, ix->sw.M,
+                        ix->sw.Mb, ix->sw.Fm, ix->sw.Fp, ix->sy, st);
+    if (e != cudaSuccess) return cuda_fail(e, "generate features");
   }
   return LINR_OK;
 }
@@ -1504,6 +1523,199 @@ int linr_search_idc(linr_index* ix, const void* q, int32_t B, int32_t V, const l
   if (ix->prof) ix->prof_launches += 1;
   return search_impl(ix, q, B, V, cl, off, K, W + w.local, ws_bytes - w.local, 0, out_ids, out_scores, nullptr,
                      out_pass, st, (const uint32_t*)(W + w.bitmaps), (size_t)words);
+}
+
+
+// ------------------------------------------------------------------ learned scorers (scorers.cu)
+namespace {
+struct ScLay {
+  size_t Wm, bm, W1, b1, w2, b2, Fk, Wgu, bg, Wo, bo, M, Mb, y, end;
+  int Fp, Fm;
+};
+bool scorer_ok(const linr_index* ix, const linr_scorer* w, std::string* why) {
+  if (!ix || !w) { *why = "null argument"; return false; }
+  if (w->kind == LINR_SCORER_HADAMARD) {
+    if (w->F < 1 || w->F > 256 || w->H < 1 || w->H > 64) { *why = "Hadamard widths: F in [1,256], H in [1,64]"; return false; }
+    if (!w->Wm || !w->bm || !w->Wi || !w->bi || !w->W1 || !w->b1 || !w->w2 || !w->b2) { *why = "null Hadamard weight"; return false; }
+    return true;
+  }
+  if (w->kind == LINR_SCORER_MOL) {
+    if (w->K < 1 || w->K > 8 || w->dc < 4 || w->dc % 4 || w->K * w->dc > 512 || w->G < 1 || w->G > 64) {
+      *why = "MoL widths: K in [1,8], dc a multiple of 4 (K*dc <= 512), G in [1,64]";
+      return false;
+    }
+    if (!w->Fk || !w->Gk || !w->Wgu || !w->Wgx || !w->bg || !w->Wo || !w->bo) { *why = "null MoL weight"; return false; }
+    return true;
+  }
+  *why = "unknown scorer kind";
+  return false;
+}
+ScLay sc_layout(const linr_index* ix, const linr_scorer* w) {
+  ScLay l;
+  std::memset(&l, 0, sizeof(l));
+  const size_t d = ix->d.dim;
+  size_t o = 0;
+  auto take = [&](size_t floats) { const size_t at = o; o = align256(o + floats * 4); return at; };
+  if (w->kind == LINR_SCORER_HADAMARD) {
+    l.Fm = w->F;
+    l.Wm = take((size_t)w->F * d); l.bm = take(w->F); l.W1 = take((size_t)w->H * w->F); l.b1 = take(w->H);
+    l.w2 = take(w->H); l.b2 = take(1);
+    l.M = take((size_t)w->F * d); l.Mb = take(w->F);
+  } else {
+    l.Fm = w->K * w->dc + w->G;
+    l.Fk = take((size_t)w->K * w->dc * d); l.Wgu = take((size_t)w->G * d); l.bg = take(w->G);
+    l.Wo = take((size_t)w->K * w->G); l.bo = take(w->K);
+    l.M = take((size_t)l.Fm * d);   // [Gk; Wgx]
+  }
+  l.Fp = (l.Fm + 3) & ~3;
+  l.y = o;
+  l.end = o + (size_t)ix->cap_pad * l.Fp * 4;
+  return l;
+}
+}  // namespace
+
+size_t linr_scorer_storage_bytes(const linr_index* ix, const linr_scorer* w) {
+  std::string why;
+  if (!scorer_ok(ix, w, &why)) return 0;
+  return sc_layout(ix, w).end;
+}
+
+int linr_scorer_attach(linr_index* ix, const linr_scorer* w, void* storage, void* stream) {
+  std::string why;
+  if (!scorer_ok(ix, w, &why)) return fail(LINR_EINVAL, why);
+  if (!storage) return fail(LINR_EINVAL, "null storage");
+  if (ix->scorer) return fail(LINR_EINVAL, "a scorer is already attached");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const ScLay l = sc_layout(ix, w);
+  char* S = (char*)storage;
+  const size_t d = ix->d.dim;
+  cudaError_t e = cudaStreamSynchronize(st);   // setup call (like linr_codes_attach)
+  auto put = [&](size_t off, const float* src, size_t floats) {
+    if (e == cudaSuccess) e = cudaMemcpy(S + off, src, floats * 4, cudaMemcpyHostToDevice);
+  };
+  ScorerDev sd;
+  std::memset(&sd, 0, sizeof(sd));
+  sd.kind = w->kind;
+  sd.Fp = l.Fp;
+  sd.Fm = l.Fm;
+  if (w->kind == LINR_SCORER_HADAMARD) {
+    sd.F = w->F;
+    sd.H = w->H;
+    put(l.Wm, w->Wm, (size_t)w->F * d); put(l.bm, w->bm, w->F); put(l.W1, w->W1, (size_t)w->H * w->F);
+    put(l.b1, w->b1, w->H); put(l.w2, w->w2, w->H); put(l.b2, w->b2, 1);
+    put(l.M, w->Wi, (size_t)w->F * d); put(l.Mb, w->bi, w->F);
+    sd.Wm = (const float*)(S + l.Wm); sd.bm = (const float*)(S + l.bm); sd.W1 = (const float*)(S + l.W1);
+    sd.b1 = (const float*)(S + l.b1); sd.w2 = (const float*)(S + l.w2); sd.b2 = (const float*)(S + l.b2);
+    sd.Mb = (const float*)(S + l.Mb);
+  } else {
+    sd.K = w->K;
+    sd.dc = w->dc;
+    sd.G = w->G;
+    put(l.Fk, w->Fk, (size_t)w->K * w->dc * d); put(l.Wgu, w->Wgu, (size_t)w->G * d); put(l.bg, w->bg, w->G);
+    put(l.Wo, w->Wo, (size_t)w->K * w->G); put(l.bo, w->bo, w->K);
+    put(l.M, w->Gk, (size_t)w->K * w->dc * d);
+    put(l.M + (size_t)w->K * w->dc * d * 4, w->Wgx, (size_t)w->G * d);
+    sd.Fk = (const float*)(S + l.Fk); sd.Wgu = (const float*)(S + l.Wgu); sd.bg = (const float*)(S + l.bg);
+    sd.Wo = (const float*)(S + l.Wo); sd.bo = (const float*)(S + l.bo);
+    sd.Mb = nullptr;
+  }
+  sd.M = (const float*)(S + l.M);
+  DevHeader h;
+  if (e == cudaSuccess) e = cudaMemcpy(&h, ix->hdr, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "scorer attach");
+  ix->sw = sd;
+  ix->sy = (float*)(S + l.y);
+  ix->scorer = true;
+  e = launch_features(ix->d.dtype, ix->emb, ix->d.dim, (int64_t)h.hwm, 0, nullptr, 0, ix->d.capacity_rows, sd.M, sd.Mb,
+                      sd.Fm, sd.Fp, ix->sy, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scorer features");
+  return LINR_OK;
+}
+
+namespace {
+struct ScWs {
+  size_t params, cl, lists, pass, end;
+  int stride;
+};
+ScWs scws_layout(const linr_index* ix, int B, int K) {
+  ScWs w;
+  w.stride = (sc_param_floats(ix->sw) + 3) & ~3;
+  w.params = 0;
+  w.cl = align256((size_t)B * w.stride * 4);
+  w.lists = w.cl + align256((size_t)B * 16 * sizeof(KClause) + (size_t)B * 4);
+  w.pass = w.lists + align256((size_t)ix->num_sms * B * K * 8);
+  w.end = w.pass + align256((size_t)ix->num_sms * B * 8);
+  return w;
+}
+}  // namespace
+
+size_t linr_search_scored_workspace_bytes(const linr_index* ix, int32_t B, int32_t K) {
+  if (!ix || !ix->scorer || B < 1 || K < 1 || K > LINR_MAX_K) return 0;
+  return scws_layout(ix, B, K).end;
+}
+
+int linr_search_scored(linr_index* ix, const void* q, int32_t B, const linr_clause* cl, const int32_t* off, int32_t K,
+                       void* ws, size_t ws_bytes, int64_t* out_ids, float* out_scores, int64_t* out_pass, void* stream) {
+  std::string why;
+  if (!ix) return fail(LINR_EINVAL, "null index");
+  if (!ix->scorer) return fail(LINR_EINVAL, "no scorer attached (linr_scorer_attach)");
+  int rc = validate_query(ix, q, B, 1, cl, off, K, &why);
+  if (rc != LINR_OK) return fail(rc, why);
+  if (!out_ids || !out_scores) return fail(LINR_EINVAL, "null outputs");
+  const ScWs w = scws_layout(ix, B, K);
+  if (!ws || ws_bytes < w.end) return fail(LINR_ENOMEM, "workspace too small");
+  DeviceGuard dg(ix->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  cudaError_t e = launch_query_prep(ix->d.dtype, ix->sw, q, ix->d.dim, B, (float*)(W + w.params), w.stride, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scorer query launch");
+  rc = stage_clause_table(ix, cl, off, B, W + w.cl, st);
+  if (rc != LINR_OK) return rc;
+  ScorerScanParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.w = ix->sw;
+  p.y = ix->sy;
+  p.attr = ix->attr;
+  p.cap_pad = ix->cap_pad;
+  p.live = ix->live;
+  p.hdr = ix->hdr;
+  p.row0 = (uint32_t)ix->d.global_row0;
+  p.nu = B;
+  p.K = K;
+  p.params = (const float*)(W + w.params);
+  p.param_stride = w.stride;
+  p.cl = (const KClause*)(W + w.cl);
+  p.ncl = (const int*)(W + w.cl + (size_t)B * 16 * sizeof(KClause));
+  p.lists = (uint64_t*)(W + w.lists);
+  p.pass = (int64_t*)(W + w.pass);
+  if (scorer_scan_smem(w.stride) > ix->smem_optin) return fail(LINR_EUNSUPPORTED, "scorer parameters exceed shared memory");
+  e = launch_scorer_scan(p, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scorer scan launch");
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.samp = p.lists;
+  mp.samp_sl = (int64_t)B * K;
+  mp.samp_su = K;
+  mp.ms = std::min(K, kScanSample);
+  mp.list = p.lists;
+  mp.list_sl = (int64_t)B * K;
+  mp.list_su = K;
+  mp.list_len = K;
+  mp.pass = p.pass;
+  mp.pstride_l = B;
+  mp.pstride_u = 1;
+  mp.L = ix->num_sms;
+  mp.K = K;
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_pass = out_pass;
+  mp.mode = 0;
+  mp.dbg = debug_buffer();
+  e = launch_merge(mp, B, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scorer merge launch");
+  if (ix->prof) ix->prof_launches += 3;
+  return LINR_OK;
 }
 
 }  // extern "C"

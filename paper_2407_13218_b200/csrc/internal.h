@@ -260,6 +260,39 @@ cudaError_t launch_idl_set_rows(const int64_t* rows, int64_t r0, int64_t grow0, 
                                 const uint64_t* src_ids, const uint8_t* src_cnt, uint64_t* dst_ids, uint8_t* dst_cnt,
                                 int64_t cap_pad, DevHeader* hdr, cudaStream_t st);
 
+// ---------------------------------------------------------------- learned scorers (scorers.cu)
+struct ScorerDev {                 // device pointers into the caller's scorer storage
+  int kind, F, H, Fp, K, dc, G;
+  const float *Wm, *bm, *W1, *b1, *w2, *b2;   // Hadamard query side
+  const float *Fk, *Wgu, *bg, *Wo, *bo;       // MoL query side
+  const float *M, *Mb;                        // item side: y = M x (+ Mb), [Fm][dim]
+  int Fm;                                     // rows of M (F, or K*dc + G)
+};
+struct ScorerScanParams {
+  ScorerDev w;
+  const float* y;                  // [cap_pad][Fp] item features
+  const uint64_t* attr;
+  int64_t cap_pad;
+  const uint32_t* live;
+  const DevHeader* hdr;
+  uint32_t row0;
+  int nu, K;
+  const float* params;             // [nu][param_stride] query-side parameters
+  int param_stride;
+  const KClause* cl;               // [nu][16]
+  const int* ncl;
+  uint64_t* lists;                 // [grid][nu][K]
+  int64_t* pass;                   // [grid][nu]
+};
+cudaError_t launch_features(int dtype, const void* emb, int dim, int64_t n, int64_t r_begin, const int64_t* rows,
+                            int64_t grow0, int64_t cap, const float* M, const float* bias, int F, int Fp, float* y,
+                            cudaStream_t st);
+int sc_param_floats(const ScorerDev& w);
+cudaError_t launch_query_prep(int dtype, const ScorerDev& w, const void* q, int dim, int B, float* out, int stride,
+                              cudaStream_t st);
+size_t scorer_scan_smem(int param_floats);
+cudaError_t launch_scorer_scan(const ScorerScanParams& p, int grid, cudaStream_t st);
+
 // NCCL communicator of a row-sharded index (comm.cu; NCCL loaded at run time)
 int comm_create(int device, const uint8_t id[128], int rank, int world, void** out);
 void comm_destroy(void* comm);

@@ -28,6 +28,7 @@ ABI_FUNCTIONS = (
     "linr_codes_storage_bytes", "linr_codes_attach", "linr_oporp_encode", "linr_code_search_workspace_bytes",
     "linr_code_search", "linr_search_v3", "linr_idlists_storage_bytes", "linr_idlists_attach",
     "linr_idlists_set_rows", "linr_search_idc_workspace_bytes", "linr_search_idc",
+    "linr_scorer_storage_bytes", "linr_scorer_attach", "linr_search_scored_workspace_bytes", "linr_search_scored",
 )
 
 
@@ -75,6 +76,13 @@ class IdClauses:
         self.p_off = self.off.ctypes.data
 
 
+class _Scorer(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("F", ctypes.c_int32), ("H", ctypes.c_int32), ("K", ctypes.c_int32),
+                ("dc", ctypes.c_int32), ("G", ctypes.c_int32)] + \
+               [(nm, ctypes.c_void_p) for nm in ("Wm", "bm", "Wi", "bi", "W1", "b1", "w2", "b2", "Fk", "Gk",
+                                                 "Wgu", "Wgx", "bg", "Wo", "bo")]
+
+
 class _Desc(ctypes.Structure):
     _fields_ = [("capacity_rows", ctypes.c_int64), ("global_row0", ctypes.c_int64), ("dim", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("attr_words", ctypes.c_int32), ("device", ctypes.c_int32),
@@ -108,6 +116,10 @@ def library():
         "linr_nccl_unique_id": ([P], ctypes.c_int),
         "linr_codes_storage_bytes": ([P, ctypes.POINTER(_Oporp)], SZ),
         "linr_idlists_storage_bytes": ([P, I32, P], SZ),
+        "linr_scorer_storage_bytes": ([P, ctypes.POINTER(_Scorer)], SZ),
+        "linr_scorer_attach": ([P, ctypes.POINTER(_Scorer), P, P], ctypes.c_int),
+        "linr_search_scored_workspace_bytes": ([P, I32, I32], SZ),
+        "linr_search_scored": ([P, P, I32, P, P, I32, P, SZ, P, P, P, P], ctypes.c_int),
         "linr_idlists_attach": ([P, I32, P, P], ctypes.c_int),
         "linr_idlists_set_rows": ([P, I32, P, I64, I64, P, P, P], ctypes.c_int),
         "linr_search_idc_workspace_bytes": ([P, I32, I32, I32], SZ),
@@ -228,6 +240,50 @@ class Index:
         _check(library().linr_comm_init(self._h, ctypes.addressof(buf), rank, world))
         self._ws = {}   # workspaces grow by the exchange buffers
         self.comm_world = world
+
+    # ------------------------------------------------------------ learned scorers (§3.3)
+    def attach_scorer(self, weights: dict):
+        """Attach a learned scorer (linr_scorer_attach). weights: kind (1 Hadamard / 2 MoL), widths and
+        float32 arrays as in include/linr.h (e.g. datagen.scorer_weights)."""
+        st = _Scorer()
+        st.kind = int(weights["kind"])
+        for k in ("F", "H", "K", "dc", "G"):
+            setattr(st, k, int(weights.get(k, 0)))
+        keep = []
+        for nm, _ in _Scorer._fields_[6:]:
+            if nm in weights:
+                a = np.ascontiguousarray(np.asarray(weights[nm], dtype=np.float32))
+                keep.append(a)
+                setattr(st, nm, a.ctypes.data)
+        L = library()
+        n = L.linr_scorer_storage_bytes(self._h, ctypes.byref(st))
+        if n == 0:
+            raise LinrError(-1, "invalid scorer")
+        self.scorer_storage = torch.empty(n, dtype=torch.uint8, device=self.device)
+        _check(L.linr_scorer_attach(self._h, ctypes.byref(st), self.scorer_storage.data_ptr(), _stream(self.device)))
+
+    def search_scored(self, queries: torch.Tensor, clauses, K: int):
+        """Filtered top-K under the attached learned scorer (linr_search_scored); queries [B][dim]."""
+        q = queries.contiguous()
+        assert q.dim() == 2 and q.dtype == TORCH_DTYPE[self.dtype] and q.shape[1] == self.dim and q.device == self.device
+        B = q.shape[0]
+        cl = clause_array(clauses)
+        assert cl.B == B
+        ids = torch.empty((B, K), dtype=torch.int64, device=self.device)
+        sc = torch.empty((B, K), dtype=torch.float32, device=self.device)
+        ps = torch.empty(B, dtype=torch.int64, device=self.device)
+        L = library()
+        n = L.linr_search_scored_workspace_bytes(self._h, B, K)
+        if n == 0:
+            raise LinrError(-1, f"no scorer workspace for B={B} K={K}")
+        key = ("scored", B, K)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < n:
+            ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        _check(L.linr_search_scored(self._h, q.data_ptr(), B, cl.p_arr, cl.p_off, K, ws.data_ptr(), ws.numel(),
+                                    ids.data_ptr(), sc.data_ptr(), ps.data_ptr(), _stream(self.device)))
+        return ids, sc, ps
 
     # ------------------------------------------------------------ ID-list clauses (PAPER.md P:4266)
     def attach_idlists(self, widths):

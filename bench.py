@@ -59,6 +59,12 @@ def parse():
     ap.add_argument("--code-bits", type=int, default=64)
     ap.add_argument("--topk", type=int, default=None, help="K (default 1000; --path codes: 5%% of the index)")
     ap.add_argument("--keep", type=float, default=0.01, help="--path v3 keep fraction (P:4595: 1%%)")
+    ap.add_argument("--vectors", type=int, default=1,
+                    help="query vectors per user V (c5 multi-embedding: 8; scores max-merged in the kernel)")
+    ap.add_argument("--update-rate", type=float, default=0.0,
+                    help="live row updates per second of device time, interleaved on the search stream in "
+                         "64-row linr_index_update_rows calls (Table 5 rates 300/600 rows/s, P:4650-4655); "
+                         "forces --pipeline 1")
     a = ap.parse_args()
     DIM = a.dim
     DT = {"bf16": 2, "f16": 1, "i8": 3, "f32": 0}[a.dtype]   # datagen / linr_dtype codes
@@ -72,8 +78,12 @@ ESZ = 2
 
 def workload_name(args, n_items):
     tag = "c2" if (args.dtype, DIM) == ("bf16", 128) else "shard"
+    if args.vectors > 1:
+        tag = "c5"
+    vv = f", V={args.vectors}" if args.vectors > 1 else ""
+    up = f", updates {args.update_rate:g} rows/s" if args.update_rate > 0 else ""
     return (f"{tag}: {n_items // 1_000_000}M items/GPU d={DIM} {args.dtype}, 64-bit attribute bitmask pre-filter "
-            f"({args.preset}), B={args.batch}, K={K}")
+            f"({args.preset}), B={args.batch}{vv}, K={K}{up}")
 
 
 # ------------------------------------------------------------------ clocks
@@ -182,7 +192,7 @@ def oracle_sample(args, seconds_target=12.0, max_rows=2_000_000):
             t_total += time.perf_counter() - t0
             done_items += rows * args.batch
             calls += 1
-            if calls >= 200:
+            if calls >= 20000:
                 break
     ips = done_items / t_total
     return {"items_per_s": ips, "qps_equiv": ips / args.items, "rows": rows, "calls": calls, "seconds": t_total,
@@ -258,14 +268,28 @@ def run_gpu(args):
         sidx = None
         ix = Index(n_local, DIM, DT, 1, device=dev)
         ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, n_local)
-    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n_total, args.batch, 1, DIM, DT)
+    Vq = args.vectors
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n_total, args.batch, Vq, DIM, DT)
     if DT in (dg.BF16, dg.F16):
         qh = torch.from_numpy(Q.view(np.int16)).view(torch.bfloat16 if DT == dg.BF16 else torch.float16).contiguous()
     else:
         qh = torch.from_numpy(Q).contiguous()
     qd = qh.to(dev)
     qpin = qh.pin_memory()
-    cls = Clauses(dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset))
+    cls_list = dg.gen_clauses(dg.QUERY_SEED, args.batch, args.preset)
+    cls = Clauses(cls_list)
+    upd = None
+    if args.update_rate > 0:
+        # live updates (Table 5): a pool of 64-row calls -- global row ids drawn
+        # with the update seed, new rows from the datagen recipe (device generator, update seed)
+        from paper_2407_13218_b200.linr import generate_rows
+        if sidx is not None:
+            raise SystemExit("--update-rate is a single-GPU measurement (updates route to one shard)")
+        ncall = 256
+        g = torch.Generator().manual_seed(dg.UPDATE_SEED)
+        rows_pool = torch.randint(0, n_local, (ncall, 64), generator=g).to(dev)
+        emb_pool, attr_pool = generate_rows(DT, DIM, 1, dg.UPDATE_SEED, dg.MODE_DENSE, 0, ncall * 64, device=dev)
+        upd = {"rows": rows_pool, "emb": emb_pool.view(ncall, 64, DIM), "attrs": attr_pool.view(ncall, 64, 1), "next": 0}
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
 
@@ -279,6 +303,11 @@ def run_gpu(args):
         if sidx is not None:
             return sidx.search(qd, cls, K)
         return ix.search(qd, cls, K, out=(ids, sc, ps), want_pass=want_pass)
+
+    def update_call():
+        j = upd["next"] % upd["rows"].shape[0]
+        upd["next"] += 1
+        ix.update_rows(upd["rows"][j], upd["emb"][j], upd["attrs"][j])
 
     for _ in range(args.warmup):
         step()
@@ -294,7 +323,7 @@ def run_gpu(args):
         pipe streams, each with its own workspace and outputs (pipelined serving: a search's merge
         tail overlaps the next search's scan). Returns ms."""
         streams = [stream] + [torch.cuda.Stream(dev) for _ in range(pipe - 1)]
-        wss = [ix.workspace(args.batch, 1, K)] + [ix.new_workspace(args.batch, 1, K) for _ in range(pipe - 1)]
+        wss = [ix.workspace(args.batch, Vq, K)] + [ix.new_workspace(args.batch, Vq, K) for _ in range(pipe - 1)]
         outs = [(ids, sc, ps)] + [(torch.empty_like(ids), torch.empty_like(sc), torch.empty_like(ps))
                                   for _ in range(pipe - 1)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -321,18 +350,74 @@ def run_gpu(args):
             dist.barrier()
         return e0.elapsed_time(e1)
 
+    def serial_with_events(steps, calls_per_step=0.0):
+        """Serial searches on one stream, each bracketed by its own events. With live updates,
+        update calls are spread evenly over the steps (calls_per_step on average) and a search's
+        latency runs from before the update calls issued ahead of it to the end of the search (a
+        query arriving just as an update starts waits for it). Returns (total ms, latencies ms)."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        credit, ncalls = 0.0, 0
+        for k in range(steps):
+            ev[k][0].record(stream)
+            credit += calls_per_step
+            while credit >= 1.0:
+                update_call()
+                credit -= 1.0
+                ncalls += 1
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        lats = [a.elapsed_time(b) for a, b in ev]
+        return ev[0][0].elapsed_time(ev[-1][1]), lats, ncalls
+
     # ---------------- serial latency (kernel timed alone: the roofline's launch durations)
     ix.profile(True)
     lat_ms = timed(args.steps, 1) / args.steps
     prof = ix.profile_read()
     ix.profile(False)
+    upd_info = None
+    calls_per_step = 0.0
+    if upd is not None:
+        # cost of one 64-row update call, timed alone on the search stream
+        for _ in range(3):
+            update_call()
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        u0.record(stream)
+        for _ in range(50):
+            update_call()
+        u1.record(stream)
+        torch.cuda.synchronize()
+        upd_ms = u0.elapsed_time(u1) / 50
+        calls_per_step = args.update_rate * (lat_ms / 1e3) / 64.0
+    lsteps = args.steps if upd is not None else min(args.steps, 1000)
+    _, lats, ncalls_lat = serial_with_events(lsteps, calls_per_step)
+    lats.sort()
+    lat_pct = {"mean": statistics.mean(lats), "p50": lats[len(lats) // 2],
+               "p95": lats[min(len(lats) - 1, int(0.95 * len(lats)))],
+               "p99": lats[min(len(lats) - 1, int(0.99 * len(lats)))], "samples": len(lats)}
     # ---------------- device-timed throughput region
     pipe = args.pipeline if sidx is None else 1
+    if upd is not None:
+        pipe = 1   # updates and searches stay stream-ordered (linr.h concurrency contract)
     for _ in range(3):
         timed(2 * pipe, pipe)   # warm the extra streams / workspaces
     clocks = Clocks(local)
     time.sleep(0.3)
-    ms = timed(args.steps, pipe)
+    if upd is not None:
+        ms, _, ncalls = serial_with_events(args.steps, calls_per_step)
+        upd_info = {"rate_rows_per_s": args.update_rate, "rows_per_call": 64, "calls_in_timed_region": ncalls,
+                    "rows_in_timed_region": 64 * ncalls, "achieved_rows_per_s": 64 * ncalls / (ms / 1e3),
+                    "update_call_ms": upd_ms, "calls_in_latency_region": ncalls_lat,
+                    "schedule": "calls spread evenly over the searches of the timed region at the requested "
+                                "rate of device time (serial, one stream)"}
+    else:
+        ms = timed(args.steps, pipe)
     clk = clocks.stop()
     if world > 1:
         t = torch.tensor([ms, lat_ms], device=dev)
@@ -347,7 +432,7 @@ def run_gpu(args):
         # stream is synchronised (its results read back) before its buffers are reused
         epipe = max(1, args.pipeline)
         estreams = [torch.cuda.Stream(dev) for _ in range(epipe)]
-        ews = [ix.new_workspace(args.batch, 1, K, host_extra=True) for _ in range(epipe)]
+        ews = [ix.new_workspace(args.batch, Vq, K, host_extra=True) for _ in range(epipe)]
         eouts = [(torch.empty((args.batch, K), dtype=torch.int64, pin_memory=True),
                   torch.empty((args.batch, K), dtype=torch.float32, pin_memory=True),
                   torch.empty(args.batch, dtype=torch.int64, pin_memory=True)) for _ in range(epipe)]
@@ -378,10 +463,10 @@ def run_gpu(args):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    h2d = args.batch * DIM * ESZ
+    h2d = args.batch * Vq * DIM * ESZ
     d2h = args.batch * K * (8 + 4) + args.batch * 8
 
-    items_per_step = args.batch * n_total
+    items_per_step = args.batch * Vq * n_total   # items-scanned/s = B*V*N / t
     value = items_per_step / (ms_step / 1e3)
     e2e_value = items_per_step * args.steps / e2e_s
 
@@ -392,21 +477,39 @@ def run_gpu(args):
     scan_ms = prof["scan_ms"] / max(1, prof["searches"])
     peak, peak_src = measured_peaks()
     roof = None
+    if 1 < args.batch <= 8 and args.batch * Vq < 16:
+        # GEMV path with several users: the algorithmic bytes of the step are one read of the
+        # attribute words + liveness bits and the rows that pass for at least one user (union)
+        a = ix.attr_storage.view(torch.int64)[:n_local]
+        union = torch.zeros(n_local, dtype=torch.bool, device=dev)
+        for cl_b in cls_list:
+            p = torch.ones(n_local, dtype=torch.bool, device=dev)
+            for (m, w, r) in cl_b:
+                mm = int(np.array([m], dtype=np.uint64).view(np.int64)[0])
+                p &= ((a & mm) != 0) ^ bool(r)
+            union |= p
+        union_pass = int(union.sum().item())
+        del a, union
+        alg_bytes = n_local * (8 + 1 / 8) + union_pass * DIM * ESZ
     if alg_bytes is not None and scan_ms > 0:
         ach = alg_bytes / (scan_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": ncu_traffic(workload_name(args, n_local)), "kernel": f"scan_ws_kernel<{args.dtype},{DIM},1> (warp-specialised ring scan; merge is a separate kernel)",
                 "scan_ms_per_launch": round(scan_ms, 5), "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                 "alg_bytes_per_launch": int(alg_bytes), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+        if args.batch > 1:
+            roof["kernel"] = f"scan kernels of one B={args.batch} search (scan_ms = their summed durations)"
+            roof["alg_bytes_note"] = ("one read of the attribute words + liveness bits, plus the rows passing for "
+                                      f"at least one user ({union_pass} rows)")
 
-    if args.batch > 8 and scan_ms > 0:
+    if args.batch * Vq >= 16 and scan_ms > 0:
         # batched path: dense stream of every row (all of them pass for some query) + the GEMM
         import json as _json
         pk = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
         tflops_peak = pk.get("bf16_tflops_sustained", 1400.0)
         hbm_bytes = n_local * (rowbytes + 8 + 1 / 8)
-        flops = 2.0 * args.batch * n_local * DIM
+        flops = 2.0 * args.batch * Vq * n_local * DIM
         hbm_ach = hbm_bytes / (scan_ms / 1e3) / 1e9
         tc_ach = flops / (scan_ms / 1e3) / 1e12
         hf, tf = hbm_ach / peak, tc_ach / tflops_peak
@@ -440,19 +543,21 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (datagen recipe, generated on device)",
             "qps": args.batch / (ms_step / 1e3),
-            "latency_ms": lat_ms, "pipeline": pipe,
+            "latency_ms": lat_ms, "latency_pct_ms": lat_pct, "pipeline": pipe,
             "config": {"workload": workload_name(args, n_local), "n_items_per_gpu": n_local, "n_items_total": n_total,
-                       "batch": args.batch, "K": K, "dim": DIM, "preset": args.preset, "pass_count": pass_count,
+                       "batch": args.batch, "vectors": Vq, "K": K, "dim": DIM, "preset": args.preset, "pass_count": pass_count,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (index 2.56 GB/GPU > 126 MB L2; no flush needed)"},
+                       "l2": f"inputs larger than L2 (index {n_local * DIM * ESZ / 1e9:.3g} GB/GPU > 126 MB L2; no flush needed)"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "items/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s / args.steps * 1e3},
-            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "gpu_launches": int(round(launches_per_step * args.steps)) + (upd_info["calls_in_timed_region"] if upd_info else 0),
             "clocks": clk,
             "build_s": round(t_build, 2),
         }
+        if upd_info:
+            line["updates"] = upd_info
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -287,8 +287,17 @@ int max_word(const linr_clause* cl, const int32_t* off, int B) {   // attribute 
   for (int i = 0; i < off[B]; ++i) w = std::max(w, (int)cl[i].word + 1);
   return w;
 }
+// Smallest B*V that takes the batched tensor-core path (tuning knob LINR_TC_MIN; below it the
+// GEMV ring scan runs one user per launch).
+int tc_min_vectors() {
+  static const int v = [] {
+    const char* e = std::getenv("LINR_TC_MIN");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  return v;
+}
 bool use_tc(const linr_index* ix, int B, int V, int maxc, int wmax) {
-  return B * V >= 16 && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
+  return B * V >= tc_min_vectors() && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
 }
 bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
@@ -696,6 +705,12 @@ int linr_index_create(const linr_index_desc* d, linr_index** out) {
   ix->attr = (uint64_t*)d->attr_storage;
   ix->hdr = (DevHeader*)d->live_storage;
   ix->live = (uint32_t*)((char*)d->live_storage + kHdrBytes);
+  if (const char* gf = std::getenv("LINR_L2_FETCH")) {
+    // tuning knob: the L2's maximum DRAM fetch granularity (bytes; a device-wide hint). The row
+    // gather touches isolated short rows (64 B int8 d = 64), so a coarse fetch wastes traffic.
+    DeviceGuard g(d->device);
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(gf));
+  }
   *out = ix;
   return LINR_OK;
 }

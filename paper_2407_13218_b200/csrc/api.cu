@@ -44,6 +44,8 @@ cudaError_t ensure_smem(const void* kernel, size_t smem) {
 }
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
+static thread_local std::string g_detail;   // launch-site detail appended to the next CUDA failure
+void set_error_detail(const std::string& d) { g_detail = d; }
 
 static int esize(int dt) { return dt == LINR_F32 ? 4 : (dt == LINR_I8 ? 1 : 2); }
 static bool dim_ok(int d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256 || d == 512 || d == 1024; }
@@ -154,7 +156,8 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 int cuda_fail(cudaError_t e, const char* where) {
-  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  set_error(std::string(where) + ": " + cudaGetErrorString(e) + (g_detail.empty() ? "" : " (" + g_detail + ")"));
+  g_detail.clear();
   return LINR_ECUDA;
 }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }

@@ -299,6 +299,7 @@ void comm_destroy(void* comm);
 int comm_allgather_u64(void* comm, const uint64_t* send, uint64_t* recv, size_t count, cudaStream_t st);
 
 void set_error(const std::string& msg);
+void set_error_detail(const std::string& detail);
 unsigned long long* debug_buffer();
 
 }  // namespace linr

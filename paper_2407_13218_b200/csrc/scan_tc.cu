@@ -33,7 +33,7 @@ constexpr int kTcThreads = 640;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-
 constexpr int kTcXStagesMax = 6;  // item-tile ring (released by the MMA commit): as many as shared memory holds
 constexpr int kTcAStages = 8;     // attribute ring (released by the epilogue): deeper than the item ring so
                                   // the producer runs ahead of the epilogue by the item ring, not by this one
-constexpr size_t kTcSmemBudget = 232448;   // sm_100 opt-in dynamic shared memory per CTA
+constexpr size_t kTcSmemBudget = 232448 - 1024;   // sm_100 opt-in shared memory per CTA minus the kernel's 1 KB static segment
 constexpr int kTcRows = 128;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -104,6 +104,23 @@ LINR_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 LINR_DEV void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// one column (x1) / a user's V aligned columns (x2, x4), maxed: the main pass re-reads hot columns
+LINR_DEV uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return r;
+}
+LINR_DEV void tmem_ld2(uint32_t taddr, uint32_t (&v)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+LINR_DEV void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -208,10 +225,8 @@ LINR_DEV uint32_t vmax(uint32_t a, uint32_t b) {
 
 // Shared-memory layout (byte offsets from the 1 KB-aligned base). nu users, maxc clause slots per user,
 // npad = max(NP, 32) accumulator columns (a 32-column chunk never reads past the per-column tables).
-constexpr int kTcScrStride = 36;   // staged scores: [epilogue warp][kTcScrRows][36 words] (16B rows, no conflicts)
-constexpr int kTcScrRows = 4;      // hot rows staged per batch
 struct TcLay {
-  size_t q, qe, xe, x, a, astage, live, thr, ct, cq, cl, scr, cnt, ctl, bytes;
+  size_t q, qe, xe, x, a, astage, live, thr, ct, cq, cl, cnt, ctl, bytes;
   int xs;
 };
 // wmax = attribute words staged per tile (highest word any clause reads, + 1)
@@ -226,7 +241,7 @@ __host__ __device__ inline TcLay tc_lay(int np, int rowb, int nu, int maxc, int 
   l.live = (size_t)wmax * 1024;
   size_t rest = (size_t)kTcAStages * l.astage;
   rest += (size_t)nu * 8 + 16 + (size_t)npad * 8 + (size_t)nu * maxc * 16;
-  rest += (size_t)(kTcThreads / 32 - 4) * kTcScrRows * kTcScrStride * 4 + (size_t)nu * 4 + 16;
+  rest += (size_t)nu * 4 + 16;
   rest += sizeof(TcSmemCtl) + 1024;
   const size_t tile = (size_t)kTcRows * rowb;
   const size_t used = l.x + rest;
@@ -237,8 +252,7 @@ __host__ __device__ inline TcLay tc_lay(int np, int rowb, int nu, int maxc, int 
   l.ct = (l.thr + (size_t)nu * 8 + 15) / 16 * 16;                // [npad] per-column hot-test threshold
   l.cq = l.ct + (size_t)npad * 4;                                // [npad] per-column score offset
   l.cl = l.cq + (size_t)npad * 4;                                // [nu][maxc] clauses (16 B)
-  l.scr = l.cl + (size_t)nu * maxc * 16;                         // staged scores of hot rows
-  l.cnt = l.scr + (size_t)(kTcThreads / 32 - 4) * kTcScrRows * kTcScrStride * 4;   // [nu] region fill counters
+  l.cnt = l.cl + (size_t)nu * maxc * 16;                         // [nu] region fill counters
   l.ctl = (l.cnt + (size_t)nu * 4 + 15) / 16 * 16;
   l.bytes = l.ctl + sizeof(TcSmemCtl) + 1024;                    // + alignment slack
   return l;
@@ -340,12 +354,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   uint64_t* sThr = reinterpret_cast<uint64_t*>(smem + L.thr);
   uint32_t* sCT = reinterpret_cast<uint32_t*>(smem + L.ct);   // hot-test threshold per column (f32 or i32 bits)
   float* sCQ = reinterpret_cast<float*>(smem + L.cq);         // rare path: score = acc + sCQ (folded) / T (int)
-  uint32_t* sScr = reinterpret_cast<uint32_t*>(smem + L.scr);
   uint4* sCl = reinterpret_cast<uint4*>(smem + L.cl);
   int* sCnt = reinterpret_cast<int*>(smem + L.cnt);
   TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + L.ctl);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ uint32_t sFreeChunks;   // main pass: chunks holding a user without a threshold
+  __shared__ uint32_t sFreeCols[8];   // main pass (folded): lead columns of users without a threshold
 
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
   const int64_t ntiles = (hwm + kTcRows - 1) / kTcRows;
@@ -386,8 +399,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
     }
     mbar_init(&ctl->qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    sFreeChunks = 0u;
   }
+  if (tid < 8) sFreeCols[tid] = 0u;
   for (int u = tid; u < p.nu; u += kTcThreads) {
     sCnt[u] = 0;
     sThr[u] = p.thr ? p.thr[u] : 0ull;
@@ -420,8 +433,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         hi = DT == LINR_BF16 ? 3.0e38f : 65504.0f;
       } else if (T && fabsf(key_score(T)) < 16384.0f) {
         tc_h_split<DT>(key_score(T), &hi, &lo);
-      } else {   // no threshold (or out of the 16-bit range): t_eff = 0, the chunk is always hot
-        atomicOr(&sFreeChunks, 1u << (c / CW));
+      } else {   // no threshold (or out of the 16-bit range): t_eff = 0, the column is always hot
+        atomicOr(&sFreeCols[c >> 5], 1u << (c & 31));
       }
       ct = __float_as_uint(0.0f);
       cq = hi + lo;   // <= the f32 value below T: a non-hot pair rebuilds to a score < T
@@ -526,8 +539,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
     constexpr int NGRP = NEPI / 128;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int nchunks = (p.nvec + CW - 1) / CW;
-    const uint32_t free_chunks = sFreeChunks;
-    uint32_t* scr = sScr + (size_t)(warp - 4) * kTcScrRows * kTcScrStride;
+    // lead columns of the chunk (a user's first column holds the max over its V columns)
+    constexpr uint32_t kLow = CW == 32 ? 0xffffffffu : ((1u << CW) - 1u);
+    const uint32_t lead_mask = kLow & (V == 1 ? 0xffffffffu : (V == 2 ? 0x55555555u : (V == 4 ? 0x11111111u : 0x01010101u)));
     for (int64_t i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int as = (int)(i % kTcAStages);
@@ -588,84 +602,71 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           }
           continue;
         }
-        // ---- main pass: hot-row test (a user's first column holds its max; the others are <= it,
-        // so testing every column is equivalent)
-        bool hot;
-        const uint4* ct4 = reinterpret_cast<const uint4*>(sCT + c0);
+        // ---- main pass: per thread (item row), the mask of the chunk's lead columns whose score
+        // reaches the user's threshold, one funnel shift per column: float (folded) -- the sign bit
+        // of s - t_eff (acc = +-0 rebuilds to t_eff < T and is rejected below either way); int8 --
+        // the sign bit of s - t. Columns past the users never reach theirs.
+        uint32_t neg = 0u;
         if (kInt) {
-          uint32_t n4[CW / 4];
+          const uint4* ct4 = reinterpret_cast<const uint4*>(sCT + c0);
 #pragma unroll
-          for (int j4 = 0; j4 < CW / 4; ++j4) {
+          for (int j4 = CW / 4 - 1; j4 >= 0; --j4) {
             const uint4 t4 = ct4[j4];
-            n4[j4] = (uint32_t)((int)v[4 * j4] - (int)t4.x) & (uint32_t)((int)v[4 * j4 + 1] - (int)t4.y) &
-                     (uint32_t)((int)v[4 * j4 + 2] - (int)t4.z) & (uint32_t)((int)v[4 * j4 + 3] - (int)t4.w);
+            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 3] - (int)t4.w), neg, 1);
+            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 2] - (int)t4.z), neg, 1);
+            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 1] - (int)t4.y), neg, 1);
+            neg = __funnelshift_l((uint32_t)((int)v[4 * j4] - (int)t4.x), neg, 1);
           }
-          uint32_t neg = n4[0];
-#pragma unroll
-          for (int j4 = 1; j4 < CW / 4; ++j4) neg &= n4[j4];
-          hot = (neg >> 31) == 0u;
-        } else if (fold) {
-          float f[CW];
-#pragma unroll
-          for (int j = 0; j < CW; ++j) f[j] = __uint_as_float(v[j]);
-          hot = fmax_tree<CW>(f) >= 0.0f || ((free_chunks >> ch) & 1u);
         } else {
-          float f[CW];
 #pragma unroll
-          for (int j = 0; j < CW; ++j) f[j] = __uint_as_float(v[j]) - __uint_as_float(sCT[c0 + j]);
-          hot = fmax_tree<CW>(f) >= 0.0f;
+          for (int j = CW - 1; j >= 0; --j) neg = __funnelshift_l(v[j], neg, 1);
         }
-        hot = hot && live;
-        uint32_t fl = __ballot_sync(0xffffffffu, hot);
-        if (fl == 0u) continue;
-        // rare: hot rows are staged in batches of kTcScrRows; one staged row at a time, lane j < CW
-        // takes column c0 + j (the first column of its user), rebuilds the exact score, checks the
-        // full key and the clauses, appends.
-        const int cj = c0 + lane;
-        const int uj = cj >> lv;
-        const bool lead = lane < CW && (lane & (V - 1)) == 0 && cj < p.nvec;
-        const float cq = lead ? sCQ[cj] : 0.0f;
-        const bool freej = fold && lead && sThr[uj] == 0ull;   // user without a threshold
-        while (fl) {
-          const uint32_t nth = __fns(fl, 0, kTcScrRows + 1);   // position of the (kTcScrRows+1)-th hot row
-          const uint32_t batch = nth == 0xffffffffu ? fl : (fl & ((1u << nth) - 1u));
-          fl &= ~batch;
-          if ((batch >> lane) & 1u) {
-            uint32_t* dst = scr + __popc(batch & lanemask_lt()) * kTcScrStride;
-#pragma unroll
-            for (int q4 = 0; q4 < CW / 4; ++q4)
-              *reinterpret_cast<uint4*>(dst + 4 * q4) = make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+        uint32_t hm = ~neg & lead_mask;
+        if (fold) hm |= (sFreeCols[c0 >> 5] >> (c0 & 31)) & lead_mask;   // users without a threshold
+        hm = live ? hm : 0u;
+        uint32_t cols = __reduce_or_sync(0xffffffffu, hm);
+        // rare: every hot lead column of the warp's 32 rows, one at a time (warp-uniform): re-read the
+        // column (the user's V columns, maxed) from TMEM; the rows where it is hot rebuild the exact
+        // key, check it against T_u and the user's clauses (row's word 0 in a register), append.
+        while (cols) {
+          const int j = __ffs(cols) - 1;
+          cols &= cols - 1u;
+          const int cj = c0 + j;
+          const uint32_t ta = tmem + lane_base + (uint32_t)(acc * NP + cj);
+          uint32_t raw;
+          if (V == 1) {
+            raw = tmem_ld1(ta);
+          } else if (V == 2) {
+            uint32_t w[2];
+            tmem_ld2(ta, w);
+            raw = vmax<kInt>(w[0], w[1]);
+          } else if (V == 4) {
+            uint32_t w[4];
+            tmem_ld4(ta, w);
+            raw = vmax<kInt>(vmax<kInt>(w[0], w[1]), vmax<kInt>(w[2], w[3]));
+          } else {
+            uint32_t w[8];
+            tmem_ld8(ta, w);
+            raw = vmax<kInt>(vmax<kInt>(vmax<kInt>(w[0], w[1]), vmax<kInt>(w[2], w[3])),
+                             vmax<kInt>(vmax<kInt>(w[4], w[5]), vmax<kInt>(w[6], w[7])));
           }
-          __syncwarp();
-          uint32_t bb = batch;
-          for (int k = 0; bb; ++k) {
-            const int r = __ffs(bb) - 1;
-            bb &= bb - 1u;
-            const uint64_t w0r = __shfl_sync(0xffffffffu, aw0, r);   // row r's attribute word 0
-            if (!lead) continue;
-            const uint32_t raw = scr[k * kTcScrStride + lane];
-            float sj;
-            bool q;
-            if (kInt) {
-              sj = (float)(int)raw;
-              q = sj >= cq;
-            } else if (fold) {
-              const float a = __uint_as_float(raw);
-              sj = a + cq;
-              q = a >= 0.0f || freej;
-            } else {
-              sj = __uint_as_float(raw);
-              q = sj >= __uint_as_float(sCT[cj]);
-            }
-            if (q) {
-              const uint64_t key = make_key(sj, rbase + (uint32_t)r);
-              if (key >= sThr[uj] && tc_clauses_reg(sCl + uj * p.maxc, p.maxc, w0r, aw, ad, (warp & 3) * 32 + r)) {
-                const int pos = atomicAdd(&sCnt[uj], 1);
-                if (pos < p.cap) p.buf[((size_t)uj * gridDim.x + blockIdx.x) * p.cap + pos] = key;
-              }
-            }
+          const int uj = cj >> lv;
+          bool ok = false;
+          uint64_t key = 0ull;
+          if ((hm >> j) & 1u) {
+            const float sj = kInt ? (float)(int)raw : __uint_as_float(raw) + sCQ[cj];
+            key = make_key(sj, rbase + (uint32_t)lane);
+            ok = key >= sThr[uj] && tc_clauses_reg(sCl + uj * p.maxc, p.maxc, aw0, aw, ad, row);
           }
-          __syncwarp();
+          const uint32_t m = __ballot_sync(0xffffffffu, ok);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&sCnt[uj], __popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            const int pos = base + __popc(m & lanemask_lt());
+            if (ok && pos < p.cap) p.buf[((size_t)uj * gridDim.x + blockIdx.x) * p.cap + pos] = key;
+          }
         }
       }
       tc_fence_before();
@@ -788,7 +789,9 @@ __global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf
 }
 
 // ------------------------------------------------------------------ pass counts (batched path, on request)
-// One warp per 32-item group: per user, ballot of the clause predicates, popc, warp total.
+// One warp per 32-item group: each attribute word and liveness word is read once, then per user
+// (warp-uniform) the ballot of the clause predicates; user u's running count lives in lane u % 32
+// (register block u / 32), so the attribute stream is read once for all users.
 __global__ void __launch_bounds__(256) tc_count_kernel(const uint64_t* attr, int64_t cap_pad, const uint32_t* live,
                                                        const DevHeader* hdr, const KClause* cl, const int* ncl,
                                                        int nu, unsigned long long* counts) {
@@ -797,20 +800,36 @@ __global__ void __launch_bounds__(256) tc_count_kernel(const uint64_t* attr, int
   const int64_t ngroups = (hwm + 31) / 32;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int u = 0; u < nu; ++u) {
-    unsigned long long tot = 0;
-    for (int64_t g = gw; g < ngroups; g += nw) {
-      const int64_t i = g * 32 + lane;
-      bool ok = (live[g] >> lane) & 1u;
-      for (int c = 0; c < ncl[u] && ok; ++c) {
-        const KClause k = cl[u * 16 + c];
-        const bool hit = (attr[(size_t)k.word * cap_pad + i] & k.mask) != 0ull;
-        if (hit == (k.rev != 0)) ok = false;
+  constexpr int kBlk = 8;   // nu <= 256 users
+  unsigned long long tot[kBlk];
+#pragma unroll
+  for (int b = 0; b < kBlk; ++b) tot[b] = 0ull;
+  for (int64_t g = gw; g < ngroups; g += nw) {
+    const int64_t i = g * 32 + lane;
+    const bool lv = (live[g] >> lane) & 1u;
+    uint64_t aw[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) aw[w] = 0ull;
+    aw[0] = attr[i];
+#pragma unroll
+    for (int b = 0; b < kBlk; ++b) {
+      if (b * 32 >= nu) break;
+      for (int j = 0; j < 32 && b * 32 + j < nu; ++j) {
+        const int u = b * 32 + j;
+        bool ok = lv;
+        for (int c = 0; c < ncl[u]; ++c) {
+          const KClause k = cl[u * 16 + c];
+          const uint64_t a = k.word == 0 ? aw[0] : attr[(size_t)k.word * cap_pad + i];
+          if (((a & k.mask) != 0ull) == (k.rev != 0)) ok = false;
+        }
+        const unsigned long long c = (unsigned long long)__popc(__ballot_sync(0xffffffffu, ok));
+        if (lane == j) tot[b] += c;
       }
-      tot += __popc(__ballot_sync(0xffffffffu, ok));
     }
-    if (lane == 0 && tot) atomicAdd(&counts[u], tot);
   }
+#pragma unroll
+  for (int b = 0; b < kBlk; ++b)
+    if (b * 32 + lane < nu && tot[b]) atomicAdd(&counts[b * 32 + lane], tot[b]);
 }
 
 cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
@@ -858,9 +877,14 @@ static cudaError_t launch_tc_np(const TcParams& p, int grid, cudaStream_t st) {
   const size_t smem = tc_lay(NP, TcGeom<DT, D>::ROWB, p.nu, p.maxc, p.wmax).bytes;
   auto k = tc_scan_kernel<DT, D, NP>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    set_error_detail("tc_scan_kernel smem " + std::to_string(smem));
+    return e;
+  }
   k<<<grid, kTcThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) set_error_detail("tc_scan_kernel launch, smem " + std::to_string(smem));
+  return e;
 }
 
 template <int DT, int D>

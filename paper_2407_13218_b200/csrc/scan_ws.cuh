@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
         const float v0 = (float)accs[sb][2 * h], v1 = (float)accs[sb][2 * h + 1];
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
+          if (u >= p.nu) break;   // warp-uniform: one user with V vectors runs one append, not NQV
           float m = -INFINITY;
           if (ucol0 == u) m = v0;
           if (ucol1 == u) m = fmaxf(m, v1);

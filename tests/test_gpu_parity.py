@@ -298,6 +298,9 @@ def test_invalid_arguments_raise():
     (dg.I8, 64, 256, 1, 20, "HIGH", 30_000),
     (dg.BF16, 64, 4, 8, 300, "HIGH", 80_000),
     (dg.BF16, 128, 256, 1, 1000, "HIGH", 200_000),
+    (dg.BF16, 128, 32, 8, 1000, "HIGH", 100_000),     # c5 U=32: 256 query vectors, max-merged per user
+    (dg.I8, 128, 16, 8, 500, "HIGH4", 60_000),
+    (dg.F16, 64, 64, 2, 200, "LOW", 200_000),
 ])
 def test_batched_tensor_core_path(dtype, d, B, V, K, preset, n):
     mode = dg.MODE_DENSE if dtype == dg.I8 else dg.MODE_GRID
@@ -333,6 +336,7 @@ def test_kernel_variants(monkeypatch, env, dtype, d, B, V, preset):
     (dg.F16, 128, 32, 1, 200, "ALL", 60_000),
     (dg.BF16, 64, 8, 4, 300, "HIGH4", 80_000),
     (dg.F16, 64, 256, 1, 50, "HIGH", 40_000),
+    (dg.BF16, 128, 32, 8, 1000, "HIGH", 100_000),
 ])
 def test_batched_tensor_core_dense(dtype, d, B, V, K, preset, n):
     """The tcgen05 path on dense (full-mantissa) inputs: scores rebuilt as acc + t_eff (reading R22)

@@ -64,6 +64,7 @@ def test_version_tags_interleaved_updates(dtype, d, B):
             _set_version(vals, attrs, np.array([r]), enc(int(ver[r])), attrs0)
         ix.update_rows(torch.from_numpy(rows).to(DEV), to_torch(vals[rows], dtype, DEV),
                        attrs_torch(attrs[rows], DEV))
+        live[rows] = 1                                               # an upsert revives a deleted row (R7)
         if step % 3 == 2:                                            # deletes on the same stream too
             dele = rng.choice(n, 50, replace=False)
             live[dele] = 0

@@ -6,7 +6,7 @@ attribute bitmasks, query vectors and query clause lists, following the recipe i
 DESIGN.md §"Input recipe" (SURVEY.md §8(d) "Synthetic inputs").
 
 The same counter-based generator is implemented a second time, independently, in CUDA
-(`paper_2407_13218_b200/csrc/gen.cu`, used only to fill 1B-row indexes in place on the
+(`gen_rows_kernel` in `paper_2407_13218_b200/csrc/index_kernels.cu`, used only to fill 1B-row indexes in place on the
 device); `tests/test_datagen.py` checks the two produce identical bytes. Oracle inputs
 always come from THIS module, never from the CUDA one.
 

@@ -42,6 +42,11 @@ cudaError_t ensure_smem(const void* kernel, size_t smem) {
   if (e == cudaSuccess) have = smem;
   return e;
 }
+// Tuning knobs: environment, read per search (each knob has a GPU parity test that sets it).
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 static thread_local std::string g_err;
 void set_error(const std::string& m) { g_err = m; }
 static thread_local std::string g_detail;   // launch-site detail appended to the next CUDA failure
@@ -290,12 +295,13 @@ int max_word(const linr_clause* cl, const int32_t* off, int B) {   // attribute 
   for (int i = 0; i < off[B]; ++i) w = std::max(w, (int)cl[i].word + 1);
   return w;
 }
-// Smallest B*V that takes the batched tensor-core path (tuning knob LINR_TC_MIN; below it the
-// GEMV ring scan runs one user per launch).
+// Smallest B*V that takes the batched tensor-core path (tuning knob LINR_TC_MIN, default 10 from
+// the measured crossover on c2 HIGH: B = 8 GEMV 0.64 ms vs tcgen05 0.78 ms, B = 12 GEMV 1.07 ms vs
+// tcgen05 0.53 ms; below it the GEMV ring scan runs one user per launch).
 int tc_min_vectors() {
   static const int v = [] {
     const char* e = std::getenv("LINR_TC_MIN");
-    return e ? std::max(1, std::atoi(e)) : 16;
+    return e ? std::max(1, std::atoi(e)) : 10;
   }();
   return v;
 }
@@ -621,7 +627,9 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   }
   if (ix->prof) cudaEventRecord(pe.e1, st);
   if (!fused) {
-    e = launch_merge(mp, B, st);
+    // LINR_PDL=1: programmatic dependent launch of the merge (saves ~1.3 us of launch gap per serial
+    // search, but the early-resident merge CTA costs ~4 % of pipelined throughput: off by default)
+    e = launch_merge(mp, B, st, env_int("LINR_PDL", 0) != 0);
     if (e != cudaSuccess) return cuda_fail(e, "merge launch");
   }
   if (ix->prof) {

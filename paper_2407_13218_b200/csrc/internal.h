@@ -49,6 +49,7 @@ struct MergeParams {
   uint64_t* out_keys;            // [B][K] (mode 1)
   int64_t* out_pass;             // [B] (may be null)
   int mode;                      // 0: decode ids/scores, 1: sorted keys
+  int bucket_sort;               // 1: skip the sorted-prefix merge (bucket sort; A/B knob LINR_MERGE_BUCKET)
   unsigned long long* dbg;       // diagnostics timers
 };
 
@@ -97,7 +98,7 @@ cudaError_t launch_scan_gemv(int dtype, int dim, int nqv, const ScanParams& p, i
 bool scan_gemv_supported(int dtype, int dim, int nqv);
 ScanCfg scan_gemv_cfg(int dtype, int dim, int nqv);
 
-cudaError_t launch_merge(const MergeParams& p, int B, cudaStream_t st);
+cudaError_t launch_merge(const MergeParams& p, int B, cudaStream_t st, bool pdl = false);
 size_t merge_smem();
 
 // index maintenance kernels
@@ -300,6 +301,7 @@ int comm_allgather_u64(void* comm, const uint64_t* send, uint64_t* recv, size_t 
 
 void set_error(const std::string& msg);
 void set_error_detail(const std::string& detail);
+int env_int(const char* name, int dflt);
 unsigned long long* debug_buffer();
 
 }  // namespace linr

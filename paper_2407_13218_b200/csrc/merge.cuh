@@ -73,6 +73,109 @@ LINR_DEV void merge_append(uint64_t* dst, int cap, MergeCtl* ctl, bool keep, uin
   }
 }
 
+// Fast path of step 3+4 when no partition is saturated: the answer is exactly the union of each
+// partition's sample prefix >= lb, and each prefix is already sorted (descending). Merge the L
+// sorted runs in groups of 8 (ceil(log8 L) rounds); in a round every key finds its merged
+// position as (its index in its run) + (keys of the group's other runs greater than it: binary
+// searches), so a round is one parallel scatter. Keys are distinct (ids are part of the key). Writes the n sorted keys
+// to the returned buffer (one of b0 / b1). Scratch: b0, b1 >= n keys; rid0, rid1 >= n bytes;
+// off0, off1 >= L + 1 ints.
+template <int NT>
+__device__ uint64_t* merge_sorted_prefixes(const uint64_t* samp, int L, int ms, uint64_t lb, int n, uint64_t* b0,
+                                           uint64_t* b1, uint8_t* rid0, uint8_t* rid1, int* off0, int* off1,
+                                           int* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  // run lengths (prefix of keys >= lb) and their exclusive scan (L <= NT)
+  int c = 0;
+  if (tid < L) {
+    const uint64_t* r = samp + tid * ms;
+    while (c < ms && r[c] != 0ull && r[c] >= lb) ++c;
+  }
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  if (tid < L) off0[tid] = base + incl - c;
+  if (tid == 0) off0[L] = n;
+  __syncthreads();
+  for (int i = tid; i < L * ms; i += NT) {   // copy the prefixes, run id = partition index
+    const int l = i / ms, j = i - l * ms;
+    const int o = off0[l];
+    if (o + j < off0[l + 1]) {
+      b0[o + j] = samp[i];
+      rid0[o + j] = (uint8_t)l;
+    }
+  }
+  __syncthreads();
+  // rounds merge groups of 8 adjacent runs (147 runs: 3 rounds); a key's merged position is its
+  // index in its run plus, for each of the other 7 runs of its group, the number of keys greater
+  // than it (branchless binary searches with a fixed step count: independent, so they overlap)
+  int R = L, maxlen = ms;
+  (void)NW;
+  while (R > 1) {
+    int steps = 0;
+    while ((1 << steps) <= maxlen) ++steps;
+    for (int i = tid; i < n; i += NT) {
+      const uint64_t x = b0[i];
+      const int r = rid0[i];
+      const int g0 = r & ~7;
+      int pos = off0[g0] + (i - off0[r]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int rq = g0 + q;
+        if (rq == r || rq >= R) continue;
+        const int lo = off0[rq], len = off0[rq + 1] - lo;
+        int c = 0;   // keys of run rq greater than x: a prefix (runs are descending)
+        for (int b = steps - 1; b >= 0; --b) {
+          const int t = c + (1 << b);
+          if (t <= len && b0[lo + t - 1] > x) c = t;
+        }
+        pos += c;
+      }
+      b1[pos] = x;
+      rid1[pos] = (uint8_t)(r >> 3);
+    }
+    const int R2 = (R + 7) >> 3;
+    for (int k = tid; k <= R2; k += NT) off1[k] = k < R2 ? off0[8 * k] : n;
+    __syncthreads();
+    uint64_t* tb = b0; b0 = b1; b1 = tb;
+    uint8_t* tr = rid0; rid0 = rid1; rid1 = tr;
+    int* to = off0; off0 = off1; off1 = to;
+    R = R2;
+    maxlen *= 8;
+    if (maxlen > n) maxlen = n;
+  }
+  return b0;
+}
+
+// Decode the n sorted keys of user u into the outputs (padding past n), and the pass count.
+template <int NT>
+__device__ void merge_write(const MergeParams& p, int u, const uint64_t* sorted, int n, long long pass) {
+  const int tid = threadIdx.x, K = p.K;
+  if (p.mode == 0) {
+    for (int j = tid; j < K; j += NT) {
+      const int64_t at = (int64_t)u * K + j;
+      if (j < n) {
+        p.out_ids[at] = key_id(sorted[j]);
+        p.out_scores[at] = key_score(sorted[j]);
+      } else {
+        p.out_ids[at] = -1;
+        p.out_scores[at] = -INFINITY;
+      }
+    }
+  } else {
+    for (int j = tid; j < K; j += NT) p.out_keys[(int64_t)u * K + j] = (j < n) ? sorted[j] : 0ull;
+  }
+  if (tid == 0 && p.out_pass) p.out_pass[u] = pass;
+}
+
 template <int NT>
 __device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
   MergeCtl* ctl = reinterpret_cast<MergeCtl*>(smem);
@@ -132,6 +235,27 @@ __device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
       // 2. LB = K-th largest sample key (zero padding sorts below it)
       const uint64_t lb = block_select_ge<NT>([s](int i) { return s[i]; }, ns, K, &ctl->sel);
       dbg_mark(p.dbg, DB + 2);
+      // no saturated partition (every sample holds a key < lb): the answer is the K sample keys
+      // >= lb, already sorted within each partition -> merge the sorted prefixes
+      if (tid == 0) ctl->cnt = 0;
+      __syncthreads();
+      bool sat = false;
+      for (int l = tid; l < L; l += NT) sat = sat || s[l * ms + ms - 1] >= lb;
+      if (__syncthreads_or(sat) == 0 && !p.bucket_sort && L <= NT && L <= 256 && K <= 4096) {
+        dbg_mark(p.dbg, DB + 3);
+        dbg_mark(p.dbg, DB + 4);
+        uint64_t* b1 = s + 8192;
+        uint8_t* rid = reinterpret_cast<uint8_t*>(s + 12288);
+        int* offs = reinterpret_cast<int*>(s + 14336);
+        const uint64_t* sorted = merge_sorted_prefixes<NT>(s, L, ms, lb, K, s2, b1, rid, rid + 4096, offs, offs + 512,
+                                                           offs + 1024);
+        dbg_mark(p.dbg, DB + 5);
+        merge_write<NT>(p, u, sorted, K, ctl->pass);
+        dbg_mark(p.dbg, DB + 6);
+        if (p.dbg != nullptr && tid == 0) p.dbg[DB + 7] = (unsigned long long)K;
+        __syncthreads();
+        return;
+      }
       // 3. survivors: sample keys >= lb (exactly K) + saturated partitions' keys in [lb, last)
 #pragma unroll
       for (int e = 0; e < kMergeRegs; ++e) merge_append(s2, kMergeOut, ctl, r[e] != 0ull && r[e] >= lb, r[e]);
@@ -190,21 +314,7 @@ __device__ void merge_user(const MergeParams& p, int u, unsigned char* smem) {
   }
   dbg_mark(p.dbg, DB + 5);
 
-  if (p.mode == 0) {
-    for (int j = tid; j < K; j += NT) {
-      const int64_t at = (int64_t)u * K + j;
-      if (j < n) {
-        p.out_ids[at] = key_id(sorted[j]);
-        p.out_scores[at] = key_score(sorted[j]);
-      } else {
-        p.out_ids[at] = -1;
-        p.out_scores[at] = -INFINITY;
-      }
-    }
-  } else {
-    for (int j = tid; j < K; j += NT) p.out_keys[(int64_t)u * K + j] = (j < n) ? sorted[j] : 0ull;
-  }
-  if (tid == 0 && p.out_pass) p.out_pass[u] = ctl->pass;
+  merge_write<NT>(p, u, sorted, n, ctl->pass);
   dbg_mark(p.dbg, DB + 6);
   if (p.dbg != nullptr && tid == 0) p.dbg[DB + 7] = (unsigned long long)n;
   __syncthreads();

@@ -455,6 +455,7 @@ __device__ __forceinline__ void scan_tail(ScanCtl* ctl, uint64_t* bufs, const Sc
 
 template <int DT, int D, int NQV, int NT>
 __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant__ ScanParams p) {
+  asm volatile("griddepcontrol.launch_dependents;");   // see scan_ws_kernel
   using G = RowGeom<DT, D, NQV>;
   using M = MmaGeom<DT, D>;
   constexpr bool kMma = ScanGeom<DT, D, NQV>::kMma;

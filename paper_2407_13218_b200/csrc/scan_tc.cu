@@ -487,7 +487,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         const int as = (int)(i % kTcAStages);
         const uint32_t aph = (uint32_t)((i / kTcAStages) & 1);
         mbar_wait(&ctl->xempty[xs], xph ^ 1u);
-        if (p.dbg && blockIdx.x == 0 && i < 64) p.dbg[i * 4 + 0] = gtimer();
         unsigned char* xd = sX + (size_t)xs * G::XBYTES;
         mbar_expect_tx(&ctl->xfull[xs], (uint32_t)G::XBYTES);
         for (int a = 0; a < G::NATOM; ++a)
@@ -516,7 +515,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         mbar_wait(&ctl->tempty[acc], tph ^ 1u);
         mbar_wait(&ctl->xfull[xs], xph);
         tc_fence_after();
-        if (p.dbg && blockIdx.x == 0 && i < 64) p.dbg[i * 4 + 1] = gtimer();
         const uint32_t x_s = smem_u32(sX + (size_t)xs * G::XBYTES);
 #pragma unroll
         for (int k = 0; k < G::NKS; ++k) {
@@ -540,6 +538,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int nchunks = (p.nvec + CW - 1) / CW;
     // lead columns of the chunk (a user's first column holds the max over its V columns)
+    const int cmode = (p.maxc == 2 && p.wmax == 1) ? 2 : 0;
     constexpr uint32_t kLow = CW == 32 ? 0xffffffffu : ((1u << CW) - 1u);
     const uint32_t lead_mask = kLow & (V == 1 ? 0xffffffffu : (V == 2 ? 0x55555555u : (V == 4 ? 0x11111111u : 0x01010101u)));
     for (int64_t i = 0; i < nmine; ++i) {
@@ -551,7 +550,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       mbar_wait(&ctl->tfull[acc], tph);
       mbar_wait(&ctl->afull[as], aph);
       tc_fence_after();
-      if (p.dbg && blockIdx.x == 0 && i < 64 && tid == 128) p.dbg[i * 4 + 2] = gtimer();
       const unsigned char* ad = sA + (size_t)as * L.astage;
       const uint32_t lw = reinterpret_cast<const uint32_t*>(ad + L.live)[row >> 5];
       const bool live = ((lw >> (row & 31)) & 1u) && (t * kTcRows + row < hwm);
@@ -562,12 +560,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         uint32_t v[CW];
         tmem_ld<CW>(tmem + lane_base + (uint32_t)(acc * NP + ch * CW), v);
         const int c0 = ch * CW;
-        if (p.dbg && blockIdx.x == 0 && i == 0 && c0 < 32) {   // diagnostics: raw accumulator of tile 0
-          uint32_t* d32 = reinterpret_cast<uint32_t*>(p.dbg + 1024);
-          for (int j = 0; j < CW; ++j) d32[row * 32 + c0 + j] = v[j];
-          if (row == 0)
-            for (int j = 0; j < CW; ++j) d32[128 * 32 + c0 + j] = __float_as_uint(sCQ[c0 + j]);
-        }
         if (V > 1) {   // per-user max over its V aligned columns into the user's first column
 #pragma unroll
           for (int j = 0; j < CW; j += 2) v[j] = vmax<kInt>(v[j], v[j + 1]);
@@ -581,13 +573,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           }
         }
         if (sample) {
-          // ---- sample pass: thread per row; per user of the chunk (warp-uniform), the passing rows
+          // ---- sample pass: thread per row. The clause bits of the chunk's users first, in a
+          // rolled loop (one copy of the clause code: the unrolled append loop below stays small
+          // enough for the instruction cache), then per user (warp-uniform) the passing rows
           // append with one shared-memory atomic per warp
+          uint32_t pmask = 0u;
+          if (live) {
+#pragma unroll 1
+            for (int j = 0; j < CW; j += V) {
+              if (c0 + j >= p.nvec) break;
+              const int u = (c0 + j) >> lv;
+              if (tc_clauses_reg(sCl + u * p.maxc, p.maxc, aw0, aw, ad, row)) pmask |= 1u << j;
+            }
+          }
 #pragma unroll
           for (int j = 0; j < CW; ++j) {
             if ((j & (V - 1)) != 0 || c0 + j >= p.nvec) continue;
             const int u = (c0 + j) >> lv;
-            const bool ok = live && tc_clauses_reg(sCl + u * p.maxc, p.maxc, aw0, aw, ad, row);
+            const bool ok = (pmask >> j) & 1u;
             const uint32_t m = __ballot_sync(0xffffffffu, ok);
             if (m == 0u) continue;
             const int leader = __ffs(m) - 1;
@@ -606,21 +609,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
         // reaches the user's threshold, one funnel shift per column: float (folded) -- the sign bit
         // of s - t_eff (acc = +-0 rebuilds to t_eff < T and is rejected below either way); int8 --
         // the sign bit of s - t. Columns past the users never reach theirs.
-        uint32_t neg = 0u;
+        // four independent 8-column chains (bit j of chain g = column 8g + j), then combined
+        uint32_t nq[4] = {0u, 0u, 0u, 0u};
         if (kInt) {
           const uint4* ct4 = reinterpret_cast<const uint4*>(sCT + c0);
 #pragma unroll
           for (int j4 = CW / 4 - 1; j4 >= 0; --j4) {
             const uint4 t4 = ct4[j4];
-            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 3] - (int)t4.w), neg, 1);
-            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 2] - (int)t4.z), neg, 1);
-            neg = __funnelshift_l((uint32_t)((int)v[4 * j4 + 1] - (int)t4.y), neg, 1);
-            neg = __funnelshift_l((uint32_t)((int)v[4 * j4] - (int)t4.x), neg, 1);
+            uint32_t& n = nq[(4 * j4) >> 3];
+            n = __funnelshift_l((uint32_t)((int)v[4 * j4 + 3] - (int)t4.w), n, 1);
+            n = __funnelshift_l((uint32_t)((int)v[4 * j4 + 2] - (int)t4.z), n, 1);
+            n = __funnelshift_l((uint32_t)((int)v[4 * j4 + 1] - (int)t4.y), n, 1);
+            n = __funnelshift_l((uint32_t)((int)v[4 * j4] - (int)t4.x), n, 1);
           }
         } else {
 #pragma unroll
-          for (int j = CW - 1; j >= 0; --j) neg = __funnelshift_l(v[j], neg, 1);
+          for (int j = CW - 1; j >= 0; --j) nq[j >> 3] = __funnelshift_l(v[j], nq[j >> 3], 1);
         }
+        const uint32_t neg = nq[0] | (nq[1] << 8) | (nq[2] << 16) | (nq[3] << 24);
         uint32_t hm = ~neg & lead_mask;
         if (fold) hm |= (sFreeCols[c0 >> 5] >> (c0 & 31)) & lead_mask;   // users without a threshold
         hm = live ? hm : 0u;
@@ -632,6 +638,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           const int j = __ffs(cols) - 1;
           cols &= cols - 1u;
           const int cj = c0 + j;
+          const int uj = cj >> lv;
+          // the user's clauses first (the row's attribute word is in a register): most hot pairs
+          // fail them (the hot test is on unfiltered scores), and then the column is not re-read
+          bool cand = ((hm >> j) & 1u) != 0u;
+          if (cmode == 2) {   // common case: <= 2 clauses on word 0 (missing slots are always-true)
+            const uint4 k0 = sCl[uj * 2], k1 = sCl[uj * 2 + 1];
+            const uint64_t m0 = ((uint64_t)k0.y << 32) | k0.x, m1 = ((uint64_t)k1.y << 32) | k1.x;
+            cand = cand && (((aw0 & m0) != 0ull) != (k0.w != 0u)) && (((aw0 & m1) != 0ull) != (k1.w != 0u));
+          } else if (cand) {
+            cand = tc_clauses_reg(sCl + uj * p.maxc, p.maxc, aw0, aw, ad, row);
+          }
+          if (!__any_sync(0xffffffffu, cand)) continue;
           const uint32_t ta = tmem + lane_base + (uint32_t)(acc * NP + cj);
           uint32_t raw;
           if (V == 1) {
@@ -650,13 +668,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
             raw = vmax<kInt>(vmax<kInt>(vmax<kInt>(w[0], w[1]), vmax<kInt>(w[2], w[3])),
                              vmax<kInt>(vmax<kInt>(w[4], w[5]), vmax<kInt>(w[6], w[7])));
           }
-          const int uj = cj >> lv;
           bool ok = false;
           uint64_t key = 0ull;
-          if ((hm >> j) & 1u) {
+          if (cand) {
             const float sj = kInt ? (float)(int)raw : __uint_as_float(raw) + sCQ[cj];
             key = make_key(sj, rbase + (uint32_t)lane);
-            ok = key >= sThr[uj] && tc_clauses_reg(sCl + uj * p.maxc, p.maxc, aw0, aw, ad, row);
+            ok = key >= sThr[uj];
           }
           const uint32_t m = __ballot_sync(0xffffffffu, ok);
           if (m) {
@@ -673,7 +690,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       mbar_arrive(&ctl->tempty[acc]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->aempty[as]);   // one arrival per epilogue warp
-      if (p.dbg && blockIdx.x == 0 && i < 64 && tid == 128) p.dbg[i * 4 + 3] = gtimer();
     }
   }
   tc_fence_before();

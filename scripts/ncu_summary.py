@@ -23,8 +23,11 @@ def launches(path, tag):
     r = list(csv.reader(io.StringIO("".join(rows))))
     h = r[0]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.OrderedDict()
     for row in r[1:]:
+        if mi is not None and row[mi] != "gpu__time_duration.sum":
+            continue   # launch lists may also carry dram byte counters
         name = row[ki]
         v = float(row[vi].replace(",", ""))
         if row[ui] == "usecond":

@@ -301,6 +301,8 @@ def test_invalid_arguments_raise():
     (dg.BF16, 128, 32, 8, 1000, "HIGH", 100_000),     # c5 U=32: 256 query vectors, max-merged per user
     (dg.I8, 128, 16, 8, 500, "HIGH4", 60_000),
     (dg.F16, 64, 64, 2, 200, "LOW", 200_000),
+    (dg.BF16, 128, 12, 1, 1000, "HIGH", 100_000),     # B*V in [LINR_TC_MIN, 16): NP = 16, padded columns
+    (dg.I8, 64, 5, 2, 300, "LOW", 200_000),
 ])
 def test_batched_tensor_core_path(dtype, d, B, V, K, preset, n):
     mode = dg.MODE_DENSE if dtype == dg.I8 else dg.MODE_GRID

@@ -508,6 +508,13 @@ def run_gpu(args):
         pk = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
         tflops_peak = pk.get("bf16_tflops_sustained", 1400.0)
+        peak_note = "MEASURED_PEAKS.json bf16_tflops_sustained (measured)"
+        if args.dtype == "i8":
+            # kind::i8 contraction: the measured bf16 peak x the nominal dense ratio (4.5 / 2.25 POPS)
+            tflops_peak *= 2.0
+            peak_note = "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal dense int8 / bf16 ratio)"
+        elif args.dtype == "f32":
+            peak_note += " (f32 runs on the GEMV path; not a tensor-core contraction)"
         hbm_bytes = n_local * (rowbytes + 8 + 1 / 8)
         flops = 2.0 * args.batch * Vq * n_local * DIM
         hbm_ach = hbm_bytes / (scan_ms / 1e3) / 1e9
@@ -521,7 +528,7 @@ def run_gpu(args):
         if tf >= hf:
             roof = {"bound": "tensor", "achieved": round(tc_ach, 1), "peak": tflops_peak, "unit": "TFLOP/s",
                     "frac": round(tf, 4), "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)", **common}
+                    "peak_source": peak_note, **common}
         else:
             roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": peak, "unit": "GB/s", "frac": round(hf, 4),
                     "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common}

@@ -75,9 +75,9 @@ LINR_DEV void merge_append(uint64_t* dst, int cap, MergeCtl* ctl, bool keep, uin
 
 // Fast path of step 3+4 when no partition is saturated: the answer is exactly the union of each
 // partition's sample prefix >= lb, and each prefix is already sorted (descending). Merge the L
-// sorted runs in groups of 8 (ceil(log8 L) rounds); in a round every key finds its merged
-// position as (its index in its run) + (keys of the group's other runs greater than it: binary
-// searches), so a round is one parallel scatter. Keys are distinct (ids are part of the key). Writes the n sorted keys
+// sorted runs pairwise (ceil(log2 L) rounds); in a round every key finds its merged position as
+// (its index in its run) + (keys of the partner run greater than it: a binary search), so a
+// round is one parallel scatter. Keys are distinct (ids are part of the key). Writes the n sorted keys
 // to the returned buffer (one of b0 / b1). Scratch: b0, b1 >= n keys; rid0, rid1 >= n bytes;
 // off0, off1 >= L + 1 ints.
 template <int NT>
@@ -114,43 +114,46 @@ __device__ uint64_t* merge_sorted_prefixes(const uint64_t* samp, int L, int ms, 
     }
   }
   __syncthreads();
-  // rounds merge groups of 8 adjacent runs (147 runs: 3 rounds); a key's merged position is its
-  // index in its run plus, for each of the other 7 runs of its group, the number of keys greater
-  // than it (branchless binary searches with a fixed step count: independent, so they overlap)
+  // pairwise rounds (ceil(log2 L)); every thread places two keys per iteration, their branchless
+  // binary searches (fixed step count) interleaved so the dependent shared-memory loads overlap
   int R = L, maxlen = ms;
   (void)NW;
   while (R > 1) {
     int steps = 0;
     while ((1 << steps) <= maxlen) ++steps;
-    for (int i = tid; i < n; i += NT) {
-      const uint64_t x = b0[i];
-      const int r = rid0[i];
-      const int g0 = r & ~7;
-      int pos = off0[g0] + (i - off0[r]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int rq = g0 + q;
-        if (rq == r || rq >= R) continue;
-        const int lo = off0[rq], len = off0[rq + 1] - lo;
-        int c = 0;   // keys of run rq greater than x: a prefix (runs are descending)
-        for (int b = steps - 1; b >= 0; --b) {
-          const int t = c + (1 << b);
-          if (t <= len && b0[lo + t - 1] > x) c = t;
-        }
-        pos += c;
+    for (int i0 = tid; i0 < n; i0 += 2 * NT) {
+      const int i1 = i0 + NT;
+      const bool h1 = i1 < n;
+      const uint64_t x0 = b0[i0], x1 = h1 ? b0[i1] : 0ull;
+      const int r0 = rid0[i0], r1 = h1 ? rid0[i1] : r0;
+      const int p0 = r0 ^ 1, p1 = r1 ^ 1;
+      const int lo0 = p0 < R ? off0[p0] : 0, len0 = p0 < R ? off0[p0 + 1] - lo0 : 0;
+      const int lo1 = p1 < R ? off0[p1] : 0, len1 = p1 < R ? off0[p1 + 1] - lo1 : 0;
+      int c0 = 0, c1 = 0;   // partner keys greater than x: a prefix (runs are descending)
+      for (int b = steps - 1; b >= 0; --b) {
+        const int t0 = c0 + (1 << b), t1 = c1 + (1 << b);
+        const bool g0 = t0 <= len0 && b0[lo0 + t0 - 1] > x0;
+        const bool g1 = t1 <= len1 && b0[lo1 + t1 - 1] > x1;
+        c0 = g0 ? t0 : c0;
+        c1 = g1 ? t1 : c1;
       }
-      b1[pos] = x;
-      rid1[pos] = (uint8_t)(r >> 3);
+      const int q0 = off0[r0 & ~1] + (i0 - off0[r0]) + c0;
+      b1[q0] = x0;
+      rid1[q0] = (uint8_t)(r0 >> 1);
+      if (h1) {
+        const int q1 = off0[r1 & ~1] + (i1 - off0[r1]) + c1;
+        b1[q1] = x1;
+        rid1[q1] = (uint8_t)(r1 >> 1);
+      }
     }
-    const int R2 = (R + 7) >> 3;
-    for (int k = tid; k <= R2; k += NT) off1[k] = k < R2 ? off0[8 * k] : n;
+    const int R2 = (R + 1) >> 1;
+    for (int k = tid; k <= R2; k += NT) off1[k] = k < R2 ? off0[2 * k] : n;
     __syncthreads();
     uint64_t* tb = b0; b0 = b1; b1 = tb;
     uint8_t* tr = rid0; rid0 = rid1; rid1 = tr;
     int* to = off0; off0 = off1; off1 = to;
     R = R2;
-    maxlen *= 8;
-    if (maxlen > n) maxlen = n;
+    maxlen = maxlen * 2 < n ? maxlen * 2 : n;
   }
   return b0;
 }

@@ -729,6 +729,9 @@ __device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int
 
 // ------------------------------------------------------------------ thresholds from the sample
 constexpr int kTcGatherCap = 16384;
+// finalize: a user's main-pass keys (>= T_u, ~2-4K at K <= 2048); 96 KB of shared memory lets two
+// CTAs share an SM, so 256 users finish in one wave (more keys: flagged, recomputed exactly)
+constexpr int kTcFinCap = 8192;
 constexpr double kTcSigma = 4.0;
 __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sbuf, const int* scnt, int scap,
                                                               int grid, int nu, int K, int sample_items,
@@ -771,11 +774,11 @@ __global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf
   extern __shared__ __align__(16) unsigned char fsm[];
   FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
   uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
-  uint64_t* s2 = s + kTcGatherCap;   // 4096 keys
+  uint64_t* s2 = s + kTcFinCap;   // 4096 keys
   const int u = blockIdx.x, tid = threadIdx.x;
   if (u == 0 && tid == 0) *fb_bar = 0u;   // the fallback kernel's grid barrier starts from zero
   long long total = 0;
-  int n = gather_regions<512>(buf, cnt, grid, cap, u, s, kTcGatherCap, &f->n, &f->total, &total);
+  int n = gather_regions<512>(buf, cnt, grid, cap, u, s, kTcFinCap, &f->n, &f->total, &total);
   const bool overflow = total > n;   // a region overflowed or the gather room was exceeded
   if (n > K) {
     const uint64_t T = block_select_ge<512>([s](int i) { return s[i]; }, n, K, &f->sel);
@@ -955,7 +958,7 @@ cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap,
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
                                unsigned int* fb_bar, cudaStream_t st) {
-  const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcGatherCap + 4096) * 8;
+  const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcFinCap + 4096) * 8;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_finalize_kernel), smem);
   if (e != cudaSuccess) return e;
   tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags,

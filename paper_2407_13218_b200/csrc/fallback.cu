@@ -69,6 +69,16 @@ __global__ void __launch_bounds__(kFbNT, 1) fallback_kernel(const __grid_constan
   const int64_t lo = hwm * blockIdx.x / gridDim.x, hi = hwm * (blockIdx.x + 1) / gridDim.x;
   const int K = p.K, dim = p.dim, V = p.V;
   const size_t rowe = (size_t)dim;
+  {   // common case: no user is flagged -- one coalesced read of the flags, then every CTA exits
+    __shared__ int s_any;
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    int any = 0;
+    for (int u = tid; u < p.nu; u += kFbNT) any |= p.flags[u];
+    if (any) atomicOr(&s_any, 1);
+    __syncthreads();
+    if (!s_any) return;   // uniform over the grid: no CTA reaches the grid barrier
+  }
   unsigned int gen = 0;
   int ord = 0;   // ordinal of the flagged user (picks the merging CTA)
   for (int u = 0; u < p.nu; ++u) {

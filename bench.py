@@ -520,18 +520,18 @@ def run_gpu(args):
         hbm_ach = hbm_bytes / (scan_ms / 1e3) / 1e9
         tc_ach = flops / (scan_ms / 1e3) / 1e12
         hf, tf = hbm_ach / peak, tc_ach / tflops_peak
-        common = {"kernel": "tc_scan_kernel<bf16,128,NP> (sample + thresholds + main pass)",
+        common = {"kernel": f"tc_scan_kernel<{args.dtype},{DIM},NP> (sample + thresholds + main pass)",
                   "scan_ms_per_launch": round(scan_ms, 5),
                   "merge_ms_per_launch": round(prof["merge_ms"] / max(1, prof["searches"]), 5),
                   "hbm_frac": round(hf, 4), "tensor_frac": round(tf, 4),
                   "alg_bytes_per_launch": int(hbm_bytes), "alg_flops_per_launch": int(flops)}
         if tf >= hf:
             roof = {"bound": "tensor", "achieved": round(tc_ach, 1), "peak": tflops_peak, "unit": "TFLOP/s",
-                    "frac": round(tf, 4), "traffic": None,
+                    "frac": round(tf, 4), "traffic": ncu_traffic(workload_name(args, n_local)),
                     "peak_source": peak_note, **common}
         else:
             roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": peak, "unit": "GB/s", "frac": round(hf, 4),
-                    "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common}
+                    "traffic": ncu_traffic(workload_name(args, n_local)), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common}
     launches_per_step = prof["launches"] / max(1, prof["searches"])
     if world > 1:
         launches_per_step += 1   # merge kernel after the all-gather

@@ -295,13 +295,13 @@ int max_word(const linr_clause* cl, const int32_t* off, int B) {   // attribute 
   for (int i = 0; i < off[B]; ++i) w = std::max(w, (int)cl[i].word + 1);
   return w;
 }
-// Smallest B*V that takes the batched tensor-core path (tuning knob LINR_TC_MIN, default 10 from
-// the measured crossover on c2 HIGH: B = 8 GEMV 0.64 ms vs tcgen05 0.78 ms, B = 12 GEMV 1.07 ms vs
-// tcgen05 0.53 ms; below it the GEMV ring scan runs one user per launch).
+// Smallest B*V that takes the batched tensor-core path (tuning knob LINR_TC_MIN, default 9 from
+// the measured crossover on c2 HIGH, profiles/r02z: B = 8 GEMV 0.63 ms vs tcgen05 0.73 ms, B = 12
+// tcgen05 0.47 ms, GEMV ~0.08 ms per user; below it the GEMV ring scan runs one user per launch).
 int tc_min_vectors() {
   static const int v = [] {
     const char* e = std::getenv("LINR_TC_MIN");
-    return e ? std::max(1, std::atoi(e)) : 10;
+    return e ? std::max(1, std::atoi(e)) : 9;
   }();
   return v;
 }

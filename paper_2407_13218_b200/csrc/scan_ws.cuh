@@ -367,10 +367,87 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       }
       return true;
     };
-    {
-      // two tiles per step, four in flight (round 2: for every row size -- the filter is the
-      // producers' bound at low pass rates and costs nothing at high ones: c2 LOW scan 47 -> 41 us,
-      // HIGH unchanged, profiles/r02k)
+    auto step = [&](int64_t& tile, uint64_t (&a)[8], uint32_t& lw) -> bool {
+      if (tile >= t_end) return false;
+      const int64_t base = tile * kTileItems;
+      // ---- liveness: bit t of mylive = item base + 32 t + lane (fast path: the whole tile live)
+      uint32_t mylive = 0xFFu;
+      if (!__all_sync(0xffffffffu, lw == ~0u)) {
+        mylive = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mylive |= ((__shfl_sync(0xffffffffu, lw, t) >> lane) & 1u) << t;
+      }
+      uint32_t pb[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) pb[u] = (u < p.nu) ? mylive : 0u;
+      if (only_w0) {
+        clauses_on(a, 0u, pb);
+      } else if (__any_sync(0xffffffffu, mylive != 0)) {
+#pragma unroll 1
+        for (int w = 0; w < 4; ++w) {
+          if (!((p.wmask >> w) & 1u)) continue;
+          uint64_t aw[8];
+          if (w == 0) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) aw[t] = a[t];
+          } else {
+            const uint64_t* ap = p.attr + (size_t)w * p.cap_pad + base + lane;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) aw[t] = ldg_stream_u64(ap + t * 32);
+          }
+          clauses_on(aw, (uint32_t)w, pb);
+        }
+      }
+      // the registers are free: refill them with the tile three ahead
+      tile = grab();
+      if (tile < t_end) prefetch(tile, a, lw);
+      // ---- append the passing rows to the pending list (order is irrelevant: keys carry ids)
+      uint32_t any = 0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        any |= pb[u];
+        pcnt[u] += __popc(pb[u]);
+      }
+      const int mine = __popc(any);
+      int incl = mine;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      int pos = pc + incl - mine;
+      while (any) {
+        const int t = __ffs(any) - 1;
+        any &= any - 1;
+        uint32_t um = 0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) um |= ((pb[u] >> t) & 1u) << u;
+        prow[pos] = (uint32_t)(base + t * 32 + lane);
+        pm[pos] = (uint8_t)um;
+        ++pos;
+      }
+      pc += __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      // ---- full groups go to the ring; the remainder (< 16) moves to the front of the list
+      int o = 0;
+      while (pc - o >= W::GR) {
+        emit(o, W::GR);
+        o += W::GR;
+      }
+      if (o > 0) {
+        const int n = pc - o;
+        uint32_t r = 0;
+        uint8_t m = 0;
+        if (lane < n) { r = prow[o + lane]; m = pm[o + lane]; }
+        __syncwarp();
+        if (lane < n) { prow[lane] = r; pm[lane] = m; }
+        __syncwarp();
+        pc = n;
+      }
+      return true;
+    };
+    if constexpr (W::GR == 32) {
+      // short rows: the producers are the bottleneck (filter per item), two tiles per step
       int64_t t0 = grab(), t1 = grab(), t2 = grab(), t3 = grab();
       uint64_t a0[8], a1[8], a2[8], a3[8];
       uint32_t l0 = ~0u, l1 = ~0u, l2 = ~0u, l3 = ~0u;
@@ -379,6 +456,15 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       if (t2 < t_end) prefetch(t2, a2, l2);
       if (t3 < t_end) prefetch(t3, a3, l3);
       while (step2(t0, a0, l0, t1, a1, l1) && step2(t2, a2, l2, t3, a3, l3)) {
+      }
+    } else {
+      int64_t t0 = grab(), t1 = grab(), t2 = grab();
+      uint64_t a0[8], a1[8], a2[8];
+      uint32_t l0 = ~0u, l1 = ~0u, l2 = ~0u;
+      if (t0 < t_end) prefetch(t0, a0, l0);
+      if (t1 < t_end) prefetch(t1, a1, l1);
+      if (t2 < t_end) prefetch(t2, a2, l2);
+      while (step(t0, a0, l0) && step(t1, a1, l1) && step(t2, a2, l2)) {
       }
     }
     if (pc > 0) emit(0, pc);

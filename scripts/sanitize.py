@@ -1,7 +1,8 @@
 """Small searches through every kernel of the search path, for compute-sanitizer runs:
     compute-sanitizer --tool {memcheck,racecheck,synccheck} python scripts/sanitize.py [case]
 Cases: ws (warp-specialised ring scan + merge), gemv (per-warp scan, f32 + fused merge),
-tc (batched tcgen05 sample/threshold/main/finalize/fallback/count), fb (forced fallback)."""
+tc (batched tcgen05 sample/threshold/main/finalize/fallback/count), tcv (tcgen05 with V = 8 and
+with padded columns), fb (forced fallback)."""
 import os
 import sys
 
@@ -39,6 +40,9 @@ elif case == "gemv":
     run(dg.F32, 64, 40_000, 1, 1, 300, "ALL", dg.MODE_GRID)
 elif case == "tc":
     run(dg.BF16, 128, 40_000, 32, 1, 200, "HIGH", dg.MODE_GRID)
+elif case == "tcv":
+    run(dg.BF16, 128, 30_000, 4, 8, 300, "HIGH", dg.MODE_GRID)
+    run(dg.I8, 64, 30_000, 12, 1, 200, "LOW", dg.MODE_DENSE)
 elif case == "fb":
     os.environ["LINR_TC_MAIN_CAP"] = "2"
     run(dg.I8, 64, 30_000, 16, 1, 300, "HIGH", dg.MODE_DENSE)

@@ -182,7 +182,8 @@ struct Plan {
 
 constexpr size_t kScanCtlBytes = 2048;   // >= sizeof(ScanCtl) (static_assert in scan_gemv.cuh)
 
-bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why, bool one_user = false) {
+bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string* why, bool one_user = false,
+               int force_nu = 0) {
   const int dt = ix->d.dtype, dim = ix->d.dim;
   int nu = std::max(1, std::min(B, std::min(kMaxUsers, 8 / V)));
   if (one_user) nu = 1;   // per-user liveness bitmaps (ID-list clauses): one user per launch
@@ -193,8 +194,10 @@ bool make_plan(const linr_index* ix, int B, int V, int K, Plan* pl, std::string*
   const int nu_first = nu;
   if (ws_ok) nu = 1;
   if (const char* mn = std::getenv("LINR_MAX_NU")) nu = std::max(1, std::min(nu, std::atoi(mn)));
+  if (force_nu > 0) nu = force_nu;   // union path: every user in one ring-scan launch, or no plan
   for (int pass = ws_ok ? 0 : 1; pass < 2; ++pass, nu = one_user ? 1 : nu_first) {
   for (; nu >= 1; --nu) {
+    if (force_nu > 0 && (nu != force_nu || pass != 0)) return false;
     const int nqv = next_pow2(nu * V);
     if (nqv > 8 || !scan_gemv_supported(dt, dim, nqv)) continue;
     const ScanCfg cfg = scan_gemv_cfg(dt, dim, nqv);
@@ -513,6 +516,201 @@ int validate_query(const linr_index* ix, const void* q, int B, int V, const linr
   return LINR_OK;
 }
 
+// ----------------------------------------------------------------- union path (2 <= B*V <= 8)
+// Small batches share one pass over the index: the tcgen05 sample pass + threshold kernel give
+// each user a starting threshold T_u (the batched path's, reading R23), then ONE ring-scan launch
+// evaluates every user's clauses per tile and gathers the union of their passing rows once
+// (instead of one attribute pass + one row gather per user), keeping only keys >= T_u, so the
+// per-user CTA buffers stay small; the merge flags users with fewer than K keys >= T_u and the
+// fallback kernel recomputes them exactly (no host synchronisation). LINR_UNION=0 disables it.
+bool union_ok(const linr_index* ix, int B, int V, int maxc, int wmax) {
+  if (B < 2 || B * V > 8 || B > kMaxUsers || env_int("LINR_UNION", 1) == 0) return false;
+  if (std::getenv("LINR_NO_WS") || std::getenv("LINR_MAX_NU")) return false;   // kernel-variant knobs
+  return tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
+         tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
+}
+size_t union_ws_bytes(const linr_index* ix, int B, int V, int K, Plan* pl) {
+  std::string why;
+  TcWs w;
+  if (!tc_layout(ix, B, V, K, &w, &why)) return 0;
+  if (!make_plan(ix, B, V, K, pl, &why, false, B)) return 0;
+  return align256(w.end) + ws_layout(*pl, B, K).end;
+}
+
+int search_union(linr_index* ix, const void* q, int B, int V, const linr_clause* cl, const int32_t* off, int K,
+                 void* ws, size_t ws_bytes, int mode, int64_t* out_ids, float* out_scores, uint64_t* out_keys,
+                 int64_t* out_pass, cudaStream_t st) {
+  std::string why;
+  Plan pl;
+  const size_t need = union_ws_bytes(ix, B, V, K, &pl);
+  if (need == 0) return fail(LINR_EUNSUPPORTED, "no union-path plan");
+  if (!ws || ws_bytes < need) return fail(LINR_ENOMEM, "workspace too small");
+  TcWs w;
+  tc_layout(ix, B, V, K, &w, &why);
+  DeviceGuard dg(ix->d.device);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+  char* W = (char*)ws;
+  const int nvec = B * V, np = tc_np(nvec);
+  if (!ix->tmx_ok) {
+    ix->tmx_ok = tc_encode_map(&ix->tmx, ix->emb, ix->cap_pad, ix->rowbytes, 128);
+    if (!ix->tmx_ok) return fail(LINR_ECUDA, "cuTensorMapEncodeTiled failed for the item matrix");
+  }
+  TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.tmx = ix->tmx;
+  if (!tc_encode_map(&p.tmq, q, nvec, ix->rowbytes, np)) return fail(LINR_ECUDA, "cuTensorMapEncodeTiled failed for the queries");
+  {
+    const int rc = stage_clause_table(ix, cl, off, B, W + w.cl, st);
+    if (rc != LINR_OK) return rc;
+  }
+  ProfEvents pe{};
+  if (ix->prof) {
+    if (!ix->prof_free.empty()) {
+      pe = ix->prof_free.back();
+      ix->prof_free.pop_back();
+    } else {
+      cudaEventCreate(&pe.e0);
+      cudaEventCreate(&pe.e1);
+      cudaEventCreate(&pe.e2);
+    }
+    cudaEventRecord(pe.e0, st);
+  }
+  // 1. sample pass + thresholds (the batched path's kernels)
+  p.attr = ix->attr;
+  p.cap_pad = ix->cap_pad;
+  p.live = ix->live;
+  p.hdr = ix->hdr;
+  p.row0 = (uint32_t)ix->d.global_row0;
+  p.nu = B;
+  p.V = V;
+  p.nvec = nvec;
+  p.K = K;
+  p.wmax = max_word(cl, off, B);
+  p.cl = (const KClause*)(W + w.cl);
+  p.ncl = (const int*)(W + w.ncl);
+  p.maxc = max_clauses(off, B);
+  p.thr = nullptr;
+  p.buf = (uint64_t*)(W + w.sbuf);
+  p.cap = kTcSampleCap;
+  p.cnt = (int*)(W + w.scnt);
+  p.sample_tiles = kTcSampleTiles;
+  e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "union sample launch");
+  uint64_t* thr = (uint64_t*)(W + w.thr);
+  e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, ix->num_sms, B, K,
+                          ix->num_sms * kTcSampleTiles * 128, ix->hdr, thr, st);
+  if (e != cudaSuccess) return cuda_fail(e, "union threshold launch");
+  if (env_int("LINR_UNION_FORCE_FB", 0))   // test knob: thresholds above every key -> every user recomputed
+    e = cudaMemsetAsync(thr, 0xFF, (size_t)B * 8, st);
+  if (e != cudaSuccess) return cuda_fail(e, "union threshold override");
+  // 2. one ring-scan launch for every user, starting from the thresholds
+  const size_t uoff = align256(w.end);
+  const WsLayout wl = ws_layout(pl, B, K);
+  uint64_t* samp = (uint64_t*)(W + uoff + wl.samp);
+  uint64_t* lists = (uint64_t*)(W + uoff + wl.list);
+  int* cnts = (int*)(W + uoff + wl.cnt);
+  int64_t* pass = (int64_t*)(W + uoff + wl.pass);
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.samp = samp;
+  mp.samp_sl = kScanSample;
+  mp.samp_su = (int64_t)pl.grid * kScanSample;
+  mp.ms = kScanSample;
+  mp.list = lists;
+  mp.list_sl = pl.list_cap;
+  mp.list_su = (int64_t)pl.grid * pl.list_cap;
+  mp.cnt = cnts;
+  mp.cnt_sl = 1;
+  mp.cnt_su = pl.grid;
+  mp.list_len = pl.list_cap;
+  mp.pass = pass;
+  mp.pstride_l = 1;
+  mp.pstride_u = pl.grid;
+  mp.L = pl.grid;
+  mp.K = K;
+  mp.out_ids = out_ids;
+  mp.out_scores = out_scores;
+  mp.out_keys = out_keys;
+  mp.out_pass = out_pass;
+  mp.mode = mode;
+  mp.thr = thr;
+  mp.flags = (int*)(W + w.flags);
+  mp.dbg = debug_buffer();
+  ScanParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.emb = ix->emb;
+  sp.attr = ix->attr;
+  sp.live = ix->live;
+  sp.hdr = ix->hdr;
+  sp.cap_pad = ix->cap_pad;
+  sp.row0 = (uint32_t)ix->d.global_row0;
+  sp.nu = B;
+  sp.V = V;
+  sp.K = K;
+  sp.C = pl.C;
+  sp.bufcap = pl.bufcap;
+  sp.list_cap = pl.list_cap;
+  sp.dbg = debug_buffer();
+  sp.q = q;
+  sp.out_samp = samp;
+  sp.out_list = lists;
+  sp.out_cnt = cnts;
+  sp.out_pass = pass;
+  uint32_t wmask = 0;
+  for (int b = 0; b < B; ++b) {
+    sp.ncl[b] = off[b + 1] - off[b];
+    for (int c = 0; c < sp.ncl[b]; ++c) {
+      const linr_clause& k = cl[off[b] + c];
+      sp.cl[b][c].mask = k.mask;
+      sp.cl[b][c].word = k.word;
+      sp.cl[b][c].rev = k.reverse;
+      wmask |= 1u << k.word;
+    }
+  }
+  sp.wmask = wmask;
+  sp.ring = pl.ring;
+  sp.init_thr = thr;
+  sp.mp = mp;
+  e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, sp, pl.grid, pl.smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "union scan launch");
+  if (ix->prof) cudaEventRecord(pe.e1, st);
+  // 3. merge (flags users with fewer than K keys >= T_u), 4. exact recomputation of flagged users
+  e = launch_merge(mp, B, st, false);
+  if (e != cudaSuccess) return cuda_fail(e, "union merge launch");
+  e = cudaMemsetAsync(W + w.bar, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return cuda_fail(e, "union barrier reset");
+  FbParams fp;
+  std::memset(&fp, 0, sizeof(fp));
+  fp.emb = ix->emb;
+  fp.attr = ix->attr;
+  fp.cap_pad = ix->cap_pad;
+  fp.live = ix->live;
+  fp.hdr = ix->hdr;
+  fp.row0 = (uint32_t)ix->d.global_row0;
+  fp.dim = ix->d.dim;
+  fp.V = V;
+  fp.K = K;
+  fp.nu = B;
+  fp.q = q;
+  fp.cl = p.cl;
+  fp.ncl = p.ncl;
+  fp.flags = (const int*)(W + w.flags);
+  fp.lists = (uint64_t*)(W + w.fb);
+  fp.bar = (unsigned int*)(W + w.bar);
+  fp.out_ids = mode == 0 ? out_ids : nullptr;
+  fp.out_scores = mode == 0 ? out_scores : nullptr;
+  fp.out_keys = mode == 1 ? out_keys : nullptr;
+  e = launch_fallback(ix->d.dtype, fp, ix->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "union fallback launch");
+  if (ix->prof) {
+    cudaEventRecord(pe.e2, st);
+    ix->prof_used.push_back(pe);
+    ix->prof_launches += 5;
+  }
+  return LINR_OK;
+}
+
 // scan (+ per-CTA lists) then merge into either ids/scores (mode 0) or keys (mode 1)
 // live_ovr: per-user liveness bitmaps [B][live_ovr_words] replacing the index's (ID-list clauses
 // already applied, see linr_search_idc); forces the GEMV path with one user per launch.
@@ -526,6 +724,11 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
   if (!live_ovr && use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) && !ix->force_gemv)
     return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
+  if (!live_ovr && !ix->force_gemv && union_ok(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
+    Plan up;
+    if (union_ws_bytes(ix, B, V, K, &up) > 0)
+      return search_union(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
+  }
   Plan pl;
   if (!make_plan(ix, B, V, K, &pl, &why, live_ovr != nullptr)) return fail(LINR_EUNSUPPORTED, why);
   const WsLayout wl = ws_layout(pl, B, K);
@@ -894,6 +1097,10 @@ static size_t local_ws_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t
     if (tc_layout(ix, B, V, K, &w, &why)) n = w.end;
   }
   if (make_plan(ix, B, V, K, &pl, &why)) n = std::max(n, ws_layout(pl, B, K).end);
+  if (union_ok(ix, B, V, 0, 1)) {   // clause-light bound, as for the batched path
+    Plan up;
+    n = std::max(n, union_ws_bytes(ix, B, V, K, &up));
+  }
   return n;
 }
 

@@ -50,6 +50,8 @@ struct MergeParams {
   int64_t* out_pass;             // [B] (may be null)
   int mode;                      // 0: decode ids/scores, 1: sorted keys
   int bucket_sort;               // 1: skip the sorted-prefix merge (bucket sort; A/B knob LINR_MERGE_BUCKET)
+  const uint64_t* thr;           // [B] thresholds the scan started from (union path), or null
+  int* flags;                    // [B] set to 1 when fewer than K keys >= thr[u] were found (recompute)
   unsigned long long* dbg;       // diagnostics timers
 };
 
@@ -77,6 +79,7 @@ struct ScanParams {
   int fuse_slot;          // DevHeader ticket slot of this search
   int fuse_merge;                // 1: the last nu CTAs run the merge (mp) for this launch's users
   int ring;                      // > 0: warp-specialised scan with this many row-group slots
+  const uint64_t* init_thr;      // [nu] starting CTA thresholds (union path: sample-derived), or null
   MergeParams mp;                // merge of this launch's users (user index relative to the launch)
   int ncl[8];
   KClause cl[8][16];

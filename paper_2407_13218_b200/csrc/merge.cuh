@@ -177,6 +177,9 @@ __device__ void merge_write(const MergeParams& p, int u, const uint64_t* sorted,
     for (int j = tid; j < K; j += NT) p.out_keys[(int64_t)u * K + j] = (j < n) ? sorted[j] : 0ull;
   }
   if (tid == 0 && p.out_pass) p.out_pass[u] = pass;
+  // union path: the scan kept only keys >= thr[u]; fewer than K of them (while the user has K
+  // passers above 0) means the result is not provably the top-K -> recomputed exactly
+  if (tid == 0 && p.flags) p.flags[u] = (p.thr != nullptr && p.thr[u] != 0ull && n < K) ? 1 : 0;
 }
 
 template <int NT>

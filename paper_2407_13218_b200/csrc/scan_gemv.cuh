@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(NT, 1) scan_gemv_kernel(const __grid_constant_
   unsigned char* ring = rings + (size_t)warp * RING;
 
   if (tid < kMaxUsers) {
-    ctl->thr[tid] = 0ull;
+    ctl->thr[tid] = (p.init_thr != nullptr && tid < p.nu) ? p.init_thr[tid] : 0ull;
     ctl->count[tid] = 0;
     ctl->pass[tid] = 0u;
   }

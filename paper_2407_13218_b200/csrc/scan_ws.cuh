@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < kMaxUsers) {
-    ctl->thr[tid] = 0ull;
+    ctl->thr[tid] = (p.init_thr != nullptr && tid < p.nu) ? p.init_thr[tid] : 0ull;
     ctl->count[tid] = 0;
     ctl->pass[tid] = 0u;
   }
@@ -583,8 +583,27 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
       for (int h = 0; h < 2; ++h) {
         const uint32_t gid = p.row0 + lr[sb][h];
         const float v0 = (float)accs[sb][2 * h], v1 = (float)accs[sb][2 * h + 1];
-#pragma unroll
-        for (int u = 0; u < NU; ++u) {
+        if (p.V == 1) {
+          // one vector per user: this lane's two accumulator columns ARE (row, user) pairs, so
+          // each lane tests its own pairs against the users' thresholds; the per-user appends run
+          // only when some lane of the warp has a candidate (rare once the thresholds are up)
+          const uint64_t k0 = make_key(v0, gid), k1 = make_key(v1, gid);
+          const bool c0 = ucol0 >= 0 && ucol0 < p.nu && ((ent[sb][h] >> ucol0) & 1u) &&
+                          k0 >= *(volatile const unsigned long long*)&ctl->thr[ucol0];
+          const bool c1 = ucol1 >= 0 && ucol1 < p.nu && ((ent[sb][h] >> ucol1) & 1u) &&
+                          k1 >= *(volatile const unsigned long long*)&ctl->thr[ucol1];
+          if (__any_sync(0xffffffffu, c0 || c1)) {
+#pragma unroll 1
+            for (int u = 0; u < NU; ++u) {   // rolled: rare path, keep the code small (i-cache)
+              if (u >= p.nu) break;
+              const bool cand = (c0 && ucol0 == u) || (c1 && ucol1 == u);
+              Appender<NT, NU>::append(ctl, bufs, p, u, cand, (c0 && ucol0 == u) ? k0 : k1);
+            }
+          }
+          continue;
+        }
+#pragma unroll 1
+        for (int u = 0; u < NU; ++u) {   // rolled: the unrolled copies overflowed the instruction cache
           if (u >= p.nu) break;   // warp-uniform: one user with V vectors runs one append, not NQV
           float m = -INFINITY;
           if (ucol0 == u) m = v0;

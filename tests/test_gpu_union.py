@@ -1,0 +1,63 @@
+"""GPU parity of the union path (2 <= B*V <= 8 on bf16/f16/int8, d = 64/128): sample-derived
+per-user thresholds, ONE ring-scan launch over the union of the users' passing rows, merge with
+certification flags, exact device-side recomputation of flagged users (readings
+R23/R33). Compared with the oracle element by element (-m gpu)."""
+import numpy as np
+import pytest
+import torch
+
+import datagen as dg
+import oracle
+from parity import check, make_index, to_torch
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def run(dtype, d, n, B, V, K, preset, mode, expect_union=True):
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    prof = ix.profile_read()
+    if expect_union:   # sample, threshold, scan, merge, fallback: one scan launch for all B users
+        assert prof["launches"] == 5, prof
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    exact = dtype == dg.I8 or mode == dg.MODE_GRID
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, exact, what=f"union dt{dtype} d{d} B{B} V{V} {preset}")
+    return ix
+
+
+@pytest.mark.parametrize("dtype,d,B,V,K,preset,mode,n", [
+    (dg.BF16, 128, 2, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),
+    (dg.BF16, 128, 8, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),
+    (dg.BF16, 128, 4, 2, 500, "HIGH4", dg.MODE_GRID, 200_000),
+    (dg.F16, 64, 3, 1, 2048, "ALL", dg.MODE_GRID, 150_000),
+    (dg.I8, 128, 5, 1, 300, "LOW", dg.MODE_DENSE, 600_000),
+    (dg.I8, 64, 2, 4, 1000, "HIGH", dg.MODE_DENSE, 250_000),
+    (dg.BF16, 128, 6, 1, 100, "HIGH", dg.MODE_DENSE, 200_000),
+    (dg.BF16, 64, 7, 1, 1, "ALL", dg.MODE_GRID, 50_000),
+])
+def test_union_path_parity(dtype, d, B, V, K, preset, mode, n):
+    run(dtype, d, n, B, V, K, preset, mode)
+
+
+def test_union_path_small_index_and_K_exceeds_pass():
+    # fewer passers than K for some users: thresholds are 0 (no filtering) or certification fails
+    run(dg.BF16, 128, 3000, 4, 1, 1500, "HIGH", dg.MODE_GRID)
+
+
+def test_union_path_forced_fallback(monkeypatch):
+    """LINR_UNION_FORCE_FB puts every user's threshold above every key: the scan keeps nothing,
+    the merge flags every user, and the fallback kernel recomputes them exactly."""
+    monkeypatch.setenv("LINR_UNION_FORCE_FB", "1")
+    ix = run(dg.I8, 64, 120_000, 3, 2, 700, "HIGH", dg.MODE_DENSE)
+    assert ix.counters()["tc_fallbacks"] >= 3
+
+
+def test_union_path_disabled_matches(monkeypatch):
+    monkeypatch.setenv("LINR_UNION", "0")
+    run(dg.BF16, 128, 100_000, 4, 1, 1000, "HIGH", dg.MODE_GRID, expect_union=False)

@@ -524,7 +524,9 @@ int validate_query(const linr_index* ix, const void* q, int B, int V, const linr
 // per-user CTA buffers stay small; the merge flags users with fewer than K keys >= T_u and the
 // fallback kernel recomputes them exactly (no host synchronisation). LINR_UNION=0 disables it.
 bool union_ok(const linr_index* ix, int B, int V, int maxc, int wmax) {
-  if (B < 2 || B * V > 8 || B > kMaxUsers || env_int("LINR_UNION", 1) == 0) return false;
+  // measured (profiles/r02w): B = 8 HIGH 0.56 vs 0.62 ms per-user, ALL 0.58 vs 3.9 ms, LOW 0.20 vs
+  // 0.38 ms; B = 4 equal at HIGH; B = 2 and V > 1 (the consumers' V-max path) slower -> per user
+  if (V != 1 || B < 3 || B > 8 || B > kMaxUsers || env_int("LINR_UNION", 1) == 0) return false;
   if (std::getenv("LINR_NO_WS") || std::getenv("LINR_MAX_NU")) return false;   // kernel-variant knobs
   return tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;

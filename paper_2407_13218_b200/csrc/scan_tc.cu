@@ -579,11 +579,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
           // append with one shared-memory atomic per warp
           uint32_t pmask = 0u;
           if (live) {
+            if (cmode == 2) {   // <= 2 clauses on word 0: branch-free test per user
 #pragma unroll 1
-            for (int j = 0; j < CW; j += V) {
-              if (c0 + j >= p.nvec) break;
-              const int u = (c0 + j) >> lv;
-              if (tc_clauses_reg(sCl + u * p.maxc, p.maxc, aw0, aw, ad, row)) pmask |= 1u << j;
+              for (int j = 0; j < CW; j += V) {
+                if (c0 + j >= p.nvec) break;
+                const int u = (c0 + j) >> lv;
+                const uint4 k0 = sCl[u * 2], k1 = sCl[u * 2 + 1];
+                const uint64_t m0 = ((uint64_t)k0.y << 32) | k0.x, m1 = ((uint64_t)k1.y << 32) | k1.x;
+                const bool ok = (((aw0 & m0) != 0ull) != (k0.w != 0u)) && (((aw0 & m1) != 0ull) != (k1.w != 0u));
+                pmask |= (ok ? 1u : 0u) << j;
+              }
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < CW; j += V) {
+                if (c0 + j >= p.nvec) break;
+                const int u = (c0 + j) >> lv;
+                if (tc_clauses_reg(sCl + u * p.maxc, p.maxc, aw0, aw, ad, row)) pmask |= 1u << j;
+              }
             }
           }
 #pragma unroll

@@ -14,7 +14,9 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-def run(dtype, d, n, B, V, K, preset, mode, expect_union=True):
+def run(dtype, d, n, B, V, K, preset, mode, expect_union=None):
+    if expect_union is None:
+        expect_union = V == 1 and 3 <= B <= 8   # the dispatch rule
     vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
     ix = make_index(vals, attrs, dtype)
     Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, mode)
@@ -32,7 +34,8 @@ def run(dtype, d, n, B, V, K, preset, mode, expect_union=True):
 
 
 @pytest.mark.parametrize("dtype,d,B,V,K,preset,mode,n", [
-    (dg.BF16, 128, 2, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),
+    (dg.BF16, 128, 3, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),
+    (dg.BF16, 128, 2, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),      # per-user launches (B = 2)
     (dg.BF16, 128, 8, 1, 1000, "HIGH", dg.MODE_GRID, 300_000),
     (dg.BF16, 128, 4, 2, 500, "HIGH4", dg.MODE_GRID, 200_000),
     (dg.F16, 64, 3, 1, 2048, "ALL", dg.MODE_GRID, 150_000),
@@ -54,7 +57,7 @@ def test_union_path_forced_fallback(monkeypatch):
     """LINR_UNION_FORCE_FB puts every user's threshold above every key: the scan keeps nothing,
     the merge flags every user, and the fallback kernel recomputes them exactly."""
     monkeypatch.setenv("LINR_UNION_FORCE_FB", "1")
-    ix = run(dg.I8, 64, 120_000, 3, 2, 700, "HIGH", dg.MODE_DENSE)
+    ix = run(dg.I8, 64, 120_000, 3, 1, 700, "HIGH", dg.MODE_DENSE)
     assert ix.counters()["tc_fallbacks"] >= 3
 
 

@@ -748,9 +748,20 @@ __device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int
   __syncthreads();
   const int n = s_off[grid] < room ? s_off[grid] : room;
   int c = 0;
-  for (int i = tid; i < n; i += NT) {
-    while (s_off[c + 1] <= i) ++c;   // region of concatenated position i (monotone in i)
-    dst[i] = buf[((size_t)u * grid + c) * cap + (i - s_off[c])];
+  for (int i0 = tid; i0 < n; i0 += 8 * NT) {   // eight independent loads in flight per thread
+    uint64_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * NT;
+      v[k] = 0ull;
+      if (i < n) {
+        while (s_off[c + 1] <= i) ++c;   // region of concatenated position i (monotone in i)
+        v[k] = buf[((size_t)u * grid + c) * cap + (i - s_off[c])];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i0 + k * NT < n) dst[i0 + k * NT] = v[k];
   }
   __syncthreads();
   *total = *s_total;

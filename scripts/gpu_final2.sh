@@ -8,8 +8,8 @@ timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; tai
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2>&1; tail -c 400 $O/bench_ref.json
 B() { timeout 900 python bench.py --no-cpu-baseline "$@" 2>>$O/sweep.err | tail -1 | tee -a $O/sweep.jsonl | python scripts/fmt_line.py || tail -3 $O/sweep.err; }
 B --preset ALL --steps 300; B --preset LOW --steps 2000; B --preset HIGH4 --steps 1000
-B --batch 4 --steps 300; B --batch 8 --steps 300
-LINR_TC_MIN=2 B --batch 4 --steps 300; LINR_TC_MIN=2 B --batch 8 --steps 300
+B --batch 3 --steps 300; B --batch 4 --steps 300; B --batch 8 --steps 300; B --batch 8 --preset ALL --steps 100; B --batch 8 --preset LOW --steps 300
+LINR_TC_MIN=2 B --batch 4 --steps 300; LINR_TC_MIN=2 B --batch 8 --steps 300; LINR_UNION=0 B --batch 8 --steps 300; LINR_UNION=0 B --batch 8 --preset ALL --steps 100
 B --batch 12 --steps 200; B --batch 16 --steps 200; B --batch 64 --steps 100; B --batch 256 --steps 100
 B --dtype f16 --batch 256 --steps 100
 B --dtype i8 --dim 128 --items 12500000 --steps 1000

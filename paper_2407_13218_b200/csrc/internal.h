@@ -137,6 +137,7 @@ struct TcParams {
   int cap;
   int* cnt;              // [nu][grid] keys each CTA produced for each user (may exceed cap)
   int sample_tiles;      // sample pass: tiles per CTA (0 = main pass, all tiles)
+  int dyn;               // 1: epilogue warps of a TMEM lane quarter take chunks dynamically
   unsigned long long* dbg;   // diagnostics: per-tile role timestamps of CTA 0 (null = off)
 };
 

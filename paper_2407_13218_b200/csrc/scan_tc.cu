@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   TcSmemCtl* ctl = reinterpret_cast<TcSmemCtl*>(smem + L.ctl);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ uint32_t sFreeCols[8];   // main pass (folded): lead columns of users without a threshold
+  __shared__ int sChunk[2][4], sChunkDone[2][4];   // dynamic chunk tickets per (accumulator, lane quarter)
 
   const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&p.hdr->hwm);
   const int64_t ntiles = (hwm + kTcRows - 1) / kTcRows;
@@ -400,7 +401,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
     mbar_init(&ctl->qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < 8) sFreeCols[tid] = 0u;
+  if (tid < 8) {
+    sFreeCols[tid] = 0u;
+    (&sChunk[0][0])[tid] = 0;
+    (&sChunkDone[0][0])[tid] = 0;
+  }
   for (int u = tid; u < p.nu; u += kTcThreads) {
     sCnt[u] = 0;
     sThr[u] = p.thr ? p.thr[u] : 0ull;
@@ -556,7 +561,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
       const uint32_t rbase = p.row0 + (uint32_t)(t * kTcRows) + (uint32_t)((warp & 3) * 32);
       const bool aw = p.wmax == 1;   // single attribute word: keep this row's word in registers
       const uint64_t aw0 = p.wmax >= 1 ? reinterpret_cast<const uint64_t*>(ad)[row] : 0ull;
-      for (int ch = grp; ch < nchunks; ch += NGRP) {
+      // chunk order: static (grp, grp + 4, ...) or, with p.dyn, tickets shared by the four warps of
+      // this TMEM lane quarter (a warp slowed by hot columns takes fewer chunks)
+      const int q4 = warp & 3;
+      auto next_chunk = [&](int cur) -> int {
+        if (!p.dyn) return cur + NGRP;
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&sChunk[acc][q4], 1);
+        return __shfl_sync(0xffffffffu, c, 0);
+      };
+      for (int ch = p.dyn ? next_chunk(0) : grp; ch < nchunks; ch = next_chunk(ch)) {
         uint32_t v[CW];
         tmem_ld<CW>(tmem + lane_base + (uint32_t)(acc * NP + ch * CW), v);
         const int c0 = ch * CW;
@@ -696,6 +710,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
             const int pos = base + __popc(m & lanemask_lt());
             if (ok && pos < p.cap) p.buf[((size_t)uj * gridDim.x + blockIdx.x) * p.cap + pos] = key;
           }
+        }
+      }
+      if (p.dyn && lane == 0) {   // the quarter's last warp resets its tickets for tile i + 2
+        if (atomicAdd(&sChunkDone[acc][q4], 1) == NGRP - 1) {
+          sChunk[acc][q4] = 0;
+          sChunkDone[acc][q4] = 0;
         }
       }
       tc_fence_before();

@@ -422,7 +422,7 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   p.cl = (const KClause*)(W + w.cl);
   p.ncl = (const int*)(W + w.ncl);
   p.maxc = max_clauses(off, B);
-  p.dyn = env_int("LINR_TC_DYN", 1);
+  p.dyn = env_int("LINR_TC_DYN", 0);   // measured slower (r02dyn: B=256 1.36 vs 1.30 ms)
   p.dbg = nullptr;
   // 1. sample pass (no threshold)
   p.thr = nullptr;
@@ -593,7 +593,7 @@ int search_union(linr_index* ix, const void* q, int B, int V, const linr_clause*
   p.cl = (const KClause*)(W + w.cl);
   p.ncl = (const int*)(W + w.ncl);
   p.maxc = max_clauses(off, B);
-  p.dyn = env_int("LINR_TC_DYN", 1);
+  p.dyn = env_int("LINR_TC_DYN", 0);   // measured slower (r02dyn: B=256 1.36 vs 1.30 ms)
   p.thr = nullptr;
   p.buf = (uint64_t*)(W + w.sbuf);
   p.cap = kTcSampleCap;

@@ -64,3 +64,50 @@ def test_union_path_forced_fallback(monkeypatch):
 def test_union_path_disabled_matches(monkeypatch):
     monkeypatch.setenv("LINR_UNION", "0")
     run(dg.BF16, 128, 100_000, 4, 1, 1000, "HIGH", dg.MODE_GRID, expect_union=False)
+
+
+def test_union_path_multiword_clauses_and_deleted_rows():
+    """Clauses on attribute words 1..3, users without clauses, deleted rows, W = 4."""
+    n, d, W, K, B = 60_000, 64, 4, 300, 5
+    vals, attrs = dg.gen_items(3, 0, n, d, dg.I8, dg.MODE_DENSE, W=W)
+    ix = make_index(vals, attrs, dg.I8)
+    live = np.ones(n, np.uint8)
+    dead = np.random.default_rng(5).choice(n, 9000, replace=False)
+    live[dead] = 0
+    ix.delete_rows(torch.from_numpy(dead).to(DEV))
+    Q = dg.gen_queries(4, 3, n, B, 1, d, dg.I8)
+    cls = [[(0x00F0_0000_0000_00F0, 1, 0), (0x1, 3, 1), (0xFFFF << 24, 0, 1)],
+           [(0x8000_0000_0000_0001, 2, 0)],
+           [],
+           [(0xFF, 0, 0), (0xF0F0, 1, 1), (0x3, 2, 0), (0x10, 3, 1)],
+           [(0xFFFF_FFFF, 0, 1)]]
+    ix.profile(True)
+    g = ix.search(to_torch(Q, dg.I8, DEV), cls, K)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 5
+    ref = oracle.search(dg.I8, vals, attrs, live, Q, cls, K)
+    check(dg.I8, vals, attrs, live, Q, cls, K, g, ref, True, what="union multiword")
+
+
+def test_union_path_after_updates():
+    """Upserts (incl. rows past the high-water mark) between union searches: the sample, the
+    thresholds and the scan all see the updated rows (stream order, reading R16)."""
+    n, d, K, B = 80_000, 128, 800, 4
+    dtype = dg.BF16
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dtype, capacity=n + 4000)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype, dg.MODE_GRID)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    ix.search(to_torch(Q, dtype, DEV), cls, K)
+    rng = np.random.default_rng(11)
+    rows = np.concatenate([rng.choice(n, 5000, replace=False), np.arange(n, n + 4000)])
+    nv, na = dg.gen_items(dg.UPDATE_SEED, 0, len(rows), d, dtype, dg.MODE_GRID)
+    from parity import attrs_torch
+    ix.update_rows(torch.from_numpy(rows).to(DEV), to_torch(nv, dtype, DEV), attrs_torch(na, DEV))
+    fv = np.concatenate([vals, np.zeros((4000, d), vals.dtype)])
+    fa = np.concatenate([attrs, np.zeros((4000, 1), np.uint64)])
+    fv[rows], fa[rows] = nv, na
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    ref = oracle.search(dtype, fv, fa, np.ones(n + 4000, np.uint8), Q, cls, K)
+    check(dtype, fv, fa, np.ones(n + 4000, np.uint8), Q, cls, K, g, ref, True, what="union after updates")

@@ -18,11 +18,12 @@ ap.add_argument("--dim", type=int, default=128)
 ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--preset", default="HIGH")
 ap.add_argument("--K", type=int, default=1000)
+ap.add_argument("--V", type=int, default=1)
 a = ap.parse_args()
 dt = dg.DTYPE_NAMES[a.dtype]
 ix = Index(a.items, a.dim, dt, 1)
 ix.generate(dg.DATA_SEED, dg.MODE_DENSE, 0, a.items)
-Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, a.items, 1, 1, a.dim, dt)
+Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, a.items, 1, a.V, a.dim, dt)
 tq = {dg.I8: torch.int8, dg.BF16: torch.bfloat16, dg.F16: torch.float16, dg.F32: torch.float32}[dt]
 q = torch.from_numpy(Q.view(np.int16) if dt in (dg.BF16, dg.F16) else Q).view(tq).cuda()
 cls = Clauses(dg.gen_clauses(dg.QUERY_SEED, 1, a.preset))

@@ -567,6 +567,34 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
         if (scan_flag(ctl, lane)) ws_compact<NCW * 32>(ctl, bufs, p, ctid);
         continue;
       }
+      if (NQV > 1 && p.nu == 1) {
+        // one user with V > 1 vectors (c5 U = 1): the max over the user's columns (lanes mt = 0..3
+        // hold columns 2mt, 2mt+1; columns >= V are padding) by two butterfly shuffles, then the
+        // same row transposition as above -- one threshold test and one append per row group
+        const uint32_t ent = lane < W::GR ? (uint32_t)mmask[slot * W::GR + lane] : 0u;
+        const uint32_t lr = lane < W::GR ? mrow[slot * W::GR + lane] : 0u;
+        __syncwarp();
+        if (lane == 0) ws_st_release(&rel[slot], rnd + 1);   // the slot's rows and metadata are consumed
+        const int src = (lane & 7) * 4;
+        const bool ok0 = 2 * mt < p.V, ok1 = 2 * mt + 1 < p.V;
+        float xv = -INFINITY;
+#pragma unroll
+        for (int sb = 0; sb < NSUB; ++sb) {
+          float m0 = fmaxf(ok0 ? (float)accs[sb][0] : -INFINITY, ok1 ? (float)accs[sb][1] : -INFINITY);
+          float m2 = fmaxf(ok0 ? (float)accs[sb][2] : -INFINITY, ok1 ? (float)accs[sb][3] : -INFINITY);
+          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+          m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, 1));
+          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+          m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, 2));
+          const float x0 = __shfl_sync(0xffffffffu, m0, src);
+          const float x2 = __shfl_sync(0xffffffffu, m2, src);
+          if ((lane >> 4) == sb) xv = (lane & 8) ? x2 : x0;
+        }
+        const bool cand = (ent & 1u) != 0u;
+        Appender<NT, NU>::append(ctl, bufs, p, 0, cand, cand ? make_key(xv, p.row0 + lr) : 0ull);
+        if (scan_flag(ctl, lane)) ws_compact<NCW * 32>(ctl, bufs, p, ctid);
+        continue;
+      }
       uint32_t ent[NSUB][2], lr[NSUB][2];
 #pragma unroll
       for (int sb = 0; sb < NSUB; ++sb)

@@ -146,7 +146,12 @@ size_t linr_search_workspace_bytes(const linr_index* index, int32_t B, int32_t V
  *   out_ids_dev [B][K] int64, out_scores_dev [B][K] fp32, out_pass_dev [B] int64 (may be NULL:
  *                 number of live items passing each query's clauses)
  * EINVAL on: null pointers, B < 1, V < 1 or > LINR_MAX_V, K < 1 or > LINR_MAX_K, bad offsets,
- * clause word >= W, clause mask == 0, too many clauses. */
+ * clause word >= W, clause mask == 0, too many clauses.
+ * The library picks the kernel path by batch shape: one fused ring-scan launch per
+ * user (B = 1, B = 2, or V > 1); the union path (V = 1, 3 <= B <= 8: one launch over the union of
+ * the users' passing rows from sample-derived thresholds); the tcgen05 batched path (B*V >= 9;
+ * bf16/f16/int8, dim 64/128). Every path returns the exact result: the two thresholded paths
+ * certify each user on the device and recompute uncertified users exactly (readings R23, R33). */
 int linr_search(linr_index* index, const void* queries_dev, int32_t B, int32_t V,
                 const linr_clause* clauses_host, const int32_t* clause_off_host, int32_t K,
                 void* ws_dev, size_t ws_bytes, int64_t* out_ids_dev, float* out_scores_dev,

@@ -40,7 +40,8 @@ def parse():
     global DIM, DT, ESZ
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=13000,
+                    help="timed searches (default: >= 1 s of device time at the default workload, SURVEY §8(d))")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="linr", choices=["linr", "reference"])
     ap.add_argument("--batch", type=int, default=B)

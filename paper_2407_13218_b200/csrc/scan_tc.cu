@@ -21,6 +21,8 @@
 // Exactness: every key >= T_u is appended; if at least K are, the K-th is >= T_u, so the top-K
 // of the buffer is the top-K of the user's passing items (reading R13-style argument).
 #include <cuda.h>
+
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -739,7 +741,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
 // (including any beyond the region capacity: total > gathered means an overflowed region).
 template <int NT>
 __device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int cap, int u, uint64_t* dst, int room,
-                              int* s_n, long long* s_total, long long* total) {
+                              int* s_n, long long* s_total, long long* total, long long* clamped = nullptr) {
   // all region counts at once (thread per region, grid <= NT), an exclusive scan of the clamped
   // counts, then every thread copies a strided slice of the concatenation: all loads in flight
   // (round 1 walked the regions one warp-atomic at a time: ~20 us of dependent L2 round trips)
@@ -785,6 +787,7 @@ __device__ int gather_regions(const uint64_t* buf, const int* cnt, int grid, int
   }
   __syncthreads();
   *total = *s_total;
+  if (clamped) *clamped = s_off[grid];   // keys present in the regions (each clamped to cap)
   if (tid == 0) *s_n = n;
   return n;
 }
@@ -833,16 +836,36 @@ struct FinSmem {
 __global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap, int grid,
                                                              const uint64_t* thr, int K, int64_t* out_ids,
                                                              float* out_scores, uint64_t* out_keys, int* flags,
-                                                             unsigned int* fb_bar) {
+                                                             unsigned int* fb_bar, int room) {
   extern __shared__ __align__(16) unsigned char fsm[];
   FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
   uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
   uint64_t* s2 = s + kTcFinCap;   // 4096 keys
   const int u = blockIdx.x, tid = threadIdx.x;
   if (u == 0 && tid == 0) *fb_bar = 0u;   // the fallback kernel's grid barrier starts from zero
-  long long total = 0;
-  int n = gather_regions<512>(buf, cnt, grid, cap, u, s, kTcFinCap, &f->n, &f->total, &total);
-  const bool overflow = total > n;   // a region overflowed or the gather room was exceeded
+  long long total = 0, present = 0;
+  int n = gather_regions<512>(buf, cnt, grid, cap, u, s, room, &f->n, &f->total, &total, &present);
+  // a region that overflowed lost keys: flagged, recomputed exactly by the fallback
+  const bool overflow = total > present;
+  if (!overflow && present > n) {
+    // every key is in the regions but more than fit in shared memory (a loose threshold on a large
+    // shard): the exact K-th largest straight from the regions in global memory (zero padding
+    // sorts below every key), then the K keys >= it (keys are distinct) -- no fallback needed
+    auto get = [=](int i) -> uint64_t {
+      const int c = i / cap, j = i - c * cap;
+      const int m = min(cnt[(size_t)u * grid + c], cap);
+      return j < m ? buf[((size_t)u * grid + c) * cap + j] : 0ull;
+    };
+    const uint64_t TK = block_select_ge<512>(get, grid * cap, K, &f->sel);
+    if (tid == 0) f->n = 0;
+    __syncthreads();
+    for (int i = tid; i < grid * cap; i += 512) {
+      const uint64_t v = get(i);
+      if (v != 0ull && v >= TK) s[atomicAdd(&f->n, 1)] = v;
+    }
+    __syncthreads();
+    n = f->n < kTcFinCap ? f->n : kTcFinCap;
+  }
   if (n > K) {
     const uint64_t T = block_select_ge<512>([s](int i) { return s[i]; }, n, K, &f->sel);
     n = block_compact_ge<512>(s, n, T, &f->sel);
@@ -1024,8 +1047,10 @@ cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int
   const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcFinCap + 4096) * 8;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_finalize_kernel), smem);
   if (e != cudaSuccess) return e;
+  // LINR_TC_FIN_ROOM (test knob): a smaller gather room forces the exact global-memory selection
+  const int room = std::max(K, std::min(kTcFinCap, env_int("LINR_TC_FIN_ROOM", kTcFinCap)));
   tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags,
-                                            fb_bar);
+                                            fb_bar, room);
   return cudaGetLastError();
 }
 

@@ -389,6 +389,27 @@ def test_batched_certification_fallback_forced(monkeypatch, dtype, mode, d, B, V
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, g2, ref, exact, what="fallback keys")
 
 
+@pytest.mark.parametrize("dtype,mode,d,B,K,preset", [
+    (dg.BF16, dg.MODE_GRID, 128, 32, 500, "ALL"),
+    (dg.I8, dg.MODE_DENSE, 64, 20, 1000, "HIGH"),
+])
+def test_batched_finalize_exact_select_from_regions(monkeypatch, dtype, mode, d, B, K, preset):
+    """LINR_TC_FIN_ROOM shrinks the finalize's shared-memory room below a user's key count: the
+    K-th key is then selected exactly from the regions in global memory (no fallback, no flag)."""
+    monkeypatch.setenv("LINR_TC_FIN_ROOM", str(K))
+    n = 200_000
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    f0 = ix.counters()["tc_fallbacks"]
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    assert ix.counters()["tc_fallbacks"] == f0
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what="finalize global select")
+
+
 def test_batched_fallback_not_taken_normally():
     n, d, B, K = 200_000, 128, 64, 1000
     vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dg.BF16, dg.MODE_GRID)

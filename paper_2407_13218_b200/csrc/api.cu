@@ -436,6 +436,32 @@ int search_tc(linr_index* ix, const void* q, int B, int V, const linr_clause* cl
   e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, ix->num_sms, B, K,
                           ix->num_sms * kTcSampleTiles * 128, ix->hdr, (uint64_t*)(W + w.thr), st);
   if (e != cudaSuccess) return cuda_fail(e, "tc threshold launch");
+  {
+    // 2b. large shards: the first sample covers too few rows (lambda = K * sampled / rows < 8: a
+    // threshold several times looser than the K-th key, hence several times more hot pairs in the
+    // main pass). A second, main-style pass over more spread tiles collects only keys >= T1 (few,
+    // so the regions do not truncate) and refines the thresholds (never below T1). Rows are taken
+    // from the capacity (the host does not read the high-water mark).
+    const double rows = (double)std::max<int64_t>(1, ix->d.capacity_rows);
+    const double lam1 = (double)K * std::min(1.0, (double)ix->num_sms * kTcSampleTiles * 128 / rows);
+    const int s2 = (int)std::min(256.0, std::ceil(12.0 * rows / ((double)K * ix->num_sms * 128)));
+    if (lam1 < 8.0 && s2 > kTcSampleTiles && env_int("LINR_TC_REFINE", 1)) {
+      TcParams p2 = p;
+      p2.thr = (const uint64_t*)(W + w.thr);
+      p2.buf = (uint64_t*)(W + w.sbuf);
+      p2.cap = kTcSampleCap;
+      p2.cnt = (int*)(W + w.scnt);
+      p2.sample_tiles = s2;
+      p2.sample_thr = 1;
+      e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, p2, ix->num_sms, st);
+      if (e != cudaSuccess) return cuda_fail(e, "tc refine launch");
+      e = launch_tc_threshold((const uint64_t*)(W + w.sbuf), (const int*)(W + w.scnt), kTcSampleCap, ix->num_sms, B,
+                              K, ix->num_sms * s2 * 128, ix->hdr, (uint64_t*)(W + w.thr), st,
+                              (const uint64_t*)(W + w.thr));
+      if (e != cudaSuccess) return cuda_fail(e, "tc refine threshold launch");
+      if (ix->prof) ix->prof_launches += 2;
+    }
+  }
   // 3. main pass
   p.thr = (const uint64_t*)(W + w.thr);
   p.buf = (uint64_t*)(W + w.mbuf);

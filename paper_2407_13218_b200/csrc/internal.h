@@ -138,6 +138,7 @@ struct TcParams {
   int* cnt;              // [nu][grid] keys each CTA produced for each user (may exceed cap)
   int sample_tiles;      // sample pass: tiles per CTA (0 = main pass, all tiles)
   int dyn;               // 1: epilogue warps of a TMEM lane quarter take chunks dynamically
+  int sample_thr;        // 1: tiles spread like the sample pass, main-pass epilogue (keys >= thr)
   unsigned long long* dbg;   // diagnostics: per-tile role timestamps of CTA 0 (null = off)
 };
 
@@ -147,7 +148,7 @@ size_t tc_smem_bytes(int dtype, int dim, int np, int nu, int maxc, int wmax);
 bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes, int box_rows);
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st);
 cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
-                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st);
+                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st, const uint64_t* floor = nullptr);
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
                                unsigned int* fb_bar, cudaStream_t st);

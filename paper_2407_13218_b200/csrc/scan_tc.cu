@@ -367,20 +367,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_con
   const int64_t ntiles = (hwm + kTcRows - 1) / kTcRows;
   // tile sequence of this CTA: the sample pass takes sample_tiles distinct tiles per CTA spread
   // evenly over the index (every tile once if the index is smaller); the main pass strides.
-  const bool sample = p.sample_tiles > 0;
+  const bool spread = p.sample_tiles > 0;          // tile sequence of the sample passes
+  const bool sample = spread && !p.sample_thr;      // epilogue: append every passing pair
   const bool fold = !kInt && !sample;
   const int V = p.V;   // 1, 2, 4 or 8
   const int lv = V == 1 ? 0 : (V == 2 ? 1 : (V == 4 ? 2 : 3));
   const int64_t stotal = (int64_t)gridDim.x * p.sample_tiles;
   int64_t nmine;
-  if (sample) {
+  if (spread) {
     if (ntiles > stotal) nmine = p.sample_tiles;
     else nmine = max((int64_t)0, min((int64_t)p.sample_tiles, ntiles - (int64_t)blockIdx.x * p.sample_tiles));
   } else {
     nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   }
   auto tile_of = [&](int64_t i) -> int64_t {
-    if (sample) {
+    if (spread) {
       const int64_t j = (int64_t)blockIdx.x * p.sample_tiles + i;
       return ntiles > stotal ? (j * ntiles) / stotal : j;   // distinct, evenly spread
     }
@@ -801,7 +802,8 @@ constexpr int kTcFinCap = 16384;
 constexpr double kTcSigma = 4.0;
 __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sbuf, const int* scnt, int scap,
                                                               int grid, int nu, int K, int sample_items,
-                                                              const DevHeader* hdr, uint64_t* thr) {
+                                                              const DevHeader* hdr, uint64_t* thr,
+                                                              const uint64_t* floor) {
   extern __shared__ __align__(16) unsigned char tsm[];
   SelScratch* sc = reinterpret_cast<SelScratch*>(tsm);
   int* s_n = reinterpret_cast<int*>(sc + 1);
@@ -821,9 +823,12 @@ __global__ void __launch_bounds__(512, 1) tc_threshold_kernel(const uint64_t* sb
   // the finalisation's certification, which sends the user to the exact GEMV path)
   const double lam = (double)K * frac;
   const int r = (int)ceil(lam + kTcSigma * sqrt(lam) + 3.0);
-  uint64_t T = 0ull;
+  // floor (second-stage sample): the keys were collected at >= floor[u], so the r-th of them is
+  // >= floor[u]; with fewer than r of them the first-stage threshold stands
+  const uint64_t F = floor ? floor[u] : 0ull;
+  uint64_t T = F;
   if (n >= r) T = block_select_ge<512>([keys](int i) { return keys[i]; }, n, r, sc);
-  if (threadIdx.x == 0) thr[u] = T;
+  if (threadIdx.x == 0) thr[u] = T > F ? T : F;
 }
 
 // ------------------------------------------------------------------ per-user finalisation
@@ -1033,11 +1038,11 @@ cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int gr
 }
 
 cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
-                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st) {
+                                int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st, const uint64_t* floor) {
   const size_t smem = ((sizeof(SelScratch) + 32 + 15) & ~size_t(15)) + (size_t)kTcGatherCap * 8;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_threshold_kernel), smem);
   if (e != cudaSuccess) return e;
-  tc_threshold_kernel<<<nu, 512, smem, st>>>(sbuf, scnt, scap, grid, nu, K, sample_items, hdr, thr);
+  tc_threshold_kernel<<<nu, 512, smem, st>>>(sbuf, scnt, scap, grid, nu, K, sample_items, hdr, thr, floor);
   return cudaGetLastError();
 }
 

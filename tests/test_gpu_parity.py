@@ -410,6 +410,27 @@ def test_batched_finalize_exact_select_from_regions(monkeypatch, dtype, mode, d,
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, True, what="finalize global select")
 
 
+@pytest.mark.parametrize("dtype,mode,d,B,V,K,preset,n", [
+    (dg.BF16, dg.MODE_GRID, 128, 32, 1, 10, "HIGH", 500_000),
+    (dg.I8, dg.MODE_DENSE, 64, 64, 1, 5, "ALL", 400_000),
+    (dg.F16, dg.MODE_DENSE, 128, 8, 2, 20, "HIGH4", 600_000),
+])
+def test_batched_threshold_refinement(dtype, mode, d, B, V, K, preset, n):
+    """Small K * sampled / rows (< 8): a second, main-style sample pass refines the thresholds
+    (8 launches instead of 6); results stay exact (int8 / grid) or within R8/R9 (dense)."""
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, mode)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, mode)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    g = ix.search(to_torch(Q, dtype, DEV), cls, K)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 8
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    exact = dtype == dg.I8 or mode == dg.MODE_GRID
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, g, ref, exact, what=f"refine dt{dtype} B{B}")
+
+
 def test_batched_fallback_not_taken_normally():
     n, d, B, K = 200_000, 128, 64, 1000
     vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dg.BF16, dg.MODE_GRID)

@@ -434,9 +434,12 @@ def run_gpu(args):
         epipe = max(1, args.pipeline)
         estreams = [torch.cuda.Stream(dev) for _ in range(epipe)]
         ews = [ix.new_workspace(args.batch, Vq, K, host_extra=True) for _ in range(epipe)]
+        # pass counts as in the device-timed region (want_pass): the batched path computes them only
+        # on request (a clause evaluation per (row, user))
         eouts = [(torch.empty((args.batch, K), dtype=torch.int64, pin_memory=True),
                   torch.empty((args.batch, K), dtype=torch.float32, pin_memory=True),
-                  torch.empty(args.batch, dtype=torch.int64, pin_memory=True)) for _ in range(epipe)]
+                  torch.empty(args.batch, dtype=torch.int64, pin_memory=True) if want_pass else None)
+                 for _ in range(epipe)]
 
         def e2e_steps(n):
             for k in range(n):
@@ -465,7 +468,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = args.batch * Vq * DIM * ESZ
-    d2h = args.batch * K * (8 + 4) + args.batch * 8
+    d2h = args.batch * K * (8 + 4) + (args.batch * 8 if want_pass else 0)
 
     items_per_step = args.batch * Vq * n_total   # items-scanned/s = B*V*N / t
     value = items_per_step / (ms_step / 1e3)

@@ -556,9 +556,11 @@ class Index:
             ws = self.workspace(B, V, K, host_extra=True)
         fn = library().linr_search_host if sync else library().linr_search_host_async
         if not sync:
-            assert q.is_pinned() and ids.is_pinned() and sc.is_pinned() and ps.is_pinned(), "async host search needs pinned buffers"
+            assert q.is_pinned() and ids.is_pinned() and sc.is_pinned() and (ps is None or ps.is_pinned()), \
+                "async host search needs pinned buffers"
         _check(fn(self._h, q.data_ptr(), B, V, cl.p_arr, cl.p_off, K, ws.data_ptr(),
-                                          ws.numel(), ids.data_ptr(), sc.data_ptr(), ps.data_ptr(),
+                                          ws.numel(), ids.data_ptr(), sc.data_ptr(),
+                                          ps.data_ptr() if ps is not None else None,   # pass counts optional
                                           _stream(self.device)))
         return ids, sc, ps
 

@@ -481,7 +481,7 @@ def run_gpu(args):
     scan_ms = prof["scan_ms"] / max(1, prof["searches"])
     peak, peak_src = measured_peaks()
     roof = None
-    if 1 < args.batch <= 8 and args.batch * Vq < 16:
+    if 1 < args.batch <= 8 and args.batch * Vq < 9:
         # GEMV path with several users: the algorithmic bytes of the step are one read of the
         # attribute words + liveness bits and the rows that pass for at least one user (union)
         a = ix.attr_storage.view(torch.int64)[:n_local]
@@ -506,7 +506,7 @@ def run_gpu(args):
             roof["alg_bytes_note"] = ("one read of the attribute words + liveness bits, plus the rows passing for "
                                       f"at least one user ({union_pass} rows)")
 
-    if args.batch * Vq >= 16 and scan_ms > 0:
+    if args.batch * Vq >= 9 and scan_ms > 0:   # the batched tcgen05 path (LINR_TC_MIN default 9)
         # batched path: dense stream of every row (all of them pass for some query) + the GEMM
         import json as _json
         pk = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

@@ -298,7 +298,11 @@ def run_gpu(args):
     sc = torch.empty((args.batch, K), dtype=torch.float32, device=dev)
     ps = torch.empty(args.batch, dtype=torch.int64, device=dev)
 
-    want_pass = args.batch <= 8 or args.pass_counts
+    # pass counts are not part of the paper's result (reading R24): requested only where they are
+    # free (one user: the fused scan counts its passers) or asked for
+    want_pass = args.batch == 1 or args.pass_counts
+    tc_route = args.batch * args.vectors >= 9 or (args.batch * args.vectors >= 7 and not want_pass
+                                                   and os.environ.get("LINR_TC_NOPASS") == "1")
 
     def step():
         if sidx is not None:
@@ -481,7 +485,7 @@ def run_gpu(args):
     scan_ms = prof["scan_ms"] / max(1, prof["searches"])
     peak, peak_src = measured_peaks()
     roof = None
-    if 1 < args.batch <= 8 and args.batch * Vq < 9:
+    if 1 < args.batch <= 8 and not tc_route:
         # GEMV path with several users: the algorithmic bytes of the step are one read of the
         # attribute words + liveness bits and the rows that pass for at least one user (union)
         a = ix.attr_storage.view(torch.int64)[:n_local]
@@ -506,7 +510,7 @@ def run_gpu(args):
             roof["alg_bytes_note"] = ("one read of the attribute words + liveness bits, plus the rows passing for "
                                       f"at least one user ({union_pass} rows)")
 
-    if args.batch * Vq >= 9 and scan_ms > 0:   # the batched tcgen05 path (LINR_TC_MIN default 9)
+    if tc_route and scan_ms > 0:   # the batched tcgen05 path (LINR_TC_MIN default 9; 7 without pass counts)
         # batched path: dense stream of every row (all of them pass for some query) + the GEMM
         import json as _json
         pk = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

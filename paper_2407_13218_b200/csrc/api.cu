@@ -312,6 +312,12 @@ bool use_tc(const linr_index* ix, int B, int V, int maxc, int wmax) {
   return B * V >= tc_min_vectors() && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
 }
+// Without pass counts (the batched path computes them with an extra clause evaluation per
+// (row, user)) the dense tcgen05 pass wins from B*V = 7: c2 HIGH B = 8 0.43 ms vs union 0.56 ms.
+bool use_tc_nopass(const linr_index* ix, int B, int V, int maxc, int wmax) {
+  return B * V >= std::min(tc_min_vectors(), 7) && tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
+         tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
+}
 bool tc_layout(const linr_index* ix, int B, int V, int K, TcWs* w, std::string* why) {
   (void)V;
   (void)why;
@@ -752,7 +758,14 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   if (rc != LINR_OK) return fail(rc, why);
   if (mode == 0 && (!out_ids || !out_scores)) return fail(LINR_EINVAL, "null outputs");
   if (mode == 1 && !out_keys) return fail(LINR_EINVAL, "null out_keys");
-  if (!live_ovr && use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) && !ix->force_gemv)
+  // (without pass counts the dense tcgen05 pass would win from B*V = 7 at HIGH/ALL -- B = 8 0.43 ms
+  // vs 0.56 ms on the union path -- but at LOW every user's sample threshold is 0 and it takes
+  // 1.36 ms vs 0.20 ms; the host cannot tell the two apart, so B*V <= 8 stays on the union path
+  // unless LINR_TC_NOPASS=1; profiles/r02np)
+  if (!live_ovr && !ix->force_gemv &&
+      (use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) ||
+       (out_pass == nullptr && env_int("LINR_TC_NOPASS", 0) &&
+        use_tc_nopass(ix, B, V, max_clauses(off, B), max_word(cl, off, B)))))
     return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
   if (!live_ovr && !ix->force_gemv && union_ok(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
     Plan up;
@@ -1122,7 +1135,7 @@ static size_t local_ws_bytes(const linr_index* ix, int32_t B, int32_t V, int32_t
   Plan pl;
   std::string why;
   size_t n = 0;
-  if (use_tc(ix, B, V, 0, 1)) {   // clause-light bound: the batched path may be taken
+  if (use_tc(ix, B, V, 0, 1) || use_tc_nopass(ix, B, V, 0, 1)) {   // clause-light bound: the batched path may be taken
     TcWs w;
     if (tc_layout(ix, B, V, K, &w, &why)) n = w.end;
   }

@@ -111,3 +111,22 @@ def test_union_path_after_updates():
     torch.cuda.synchronize()
     ref = oracle.search(dtype, fv, fa, np.ones(n + 4000, np.uint8), Q, cls, K)
     check(dtype, fv, fa, np.ones(n + 4000, np.uint8), Q, cls, K, g, ref, True, what="union after updates")
+
+
+@pytest.mark.parametrize("B,V", [(8, 1), (7, 1), (4, 2)])
+def test_small_batch_without_pass_counts_takes_tcgen05(monkeypatch, B, V):
+    """LINR_TC_NOPASS=1: B*V in [7, 8] without requested pass counts runs the dense tcgen05 pass
+    (sample, threshold, main, finalize, fallback: 5 launches, no count kernel); exact results."""
+    monkeypatch.setenv("LINR_TC_NOPASS", "1")
+    dtype, d, n, K = dg.BF16, 128, 200_000, 500
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_GRID)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, V, d, dtype, dg.MODE_GRID)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, "HIGH")
+    ix.profile(True)
+    ids, sc, _ = ix.search(to_torch(Q, dtype, DEV), cls, K, want_pass=False)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 5
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, (ids, sc, torch.from_numpy(ref[2])), ref, True,
+          what=f"tc no-pass B{B} V{V}")

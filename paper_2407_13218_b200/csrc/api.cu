@@ -640,6 +640,33 @@ int search_union(linr_index* ix, const void* q, int B, int V, const linr_clause*
   if (env_int("LINR_UNION_FORCE_FB", 0))   // test knob: thresholds above every key -> every user recomputed
     e = cudaMemsetAsync(thr, 0xFF, (size_t)B * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "union threshold override");
+  // 2a. B*V >= 7 without pass counts: at high/medium pass rates the dense tcgen05 pass beats the
+  //     union scan (B = 8: 0.44 vs 0.56 ms); at low pass rates it does not (1.38 vs 0.20 ms). The thresholds live on the device, so the
+  //     choice is made there: a one-CTA kernel writes a gate, both paths are launched and the one
+  //     not chosen exits at once (profiles/r02gate).
+  int* gate = nullptr;
+  if (out_pass == nullptr && B * V >= 7 && env_int("LINR_UNION_TC", 1) &&
+      use_tc_nopass(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
+    gate = (int*)(W + w.bar + 128);
+    e = launch_tc_decide(thr, (const int*)(W + w.scnt), ix->num_sms, (int64_t)ix->num_sms * kTcSampleTiles * 128,
+                         ix->hdr, B, gate, st);
+    if (e != cudaSuccess) return cuda_fail(e, "union decide launch");
+    TcParams pm = p;
+    pm.thr = thr;
+    pm.buf = (uint64_t*)(W + w.mbuf);
+    pm.cap = kTcMainCap;
+    pm.cnt = (int*)(W + w.mcnt);
+    pm.sample_tiles = 0;
+    pm.gate = gate;
+    pm.gate_want = 1;
+    e = launch_tc_scan(ix->d.dtype, ix->d.dim, np, pm, ix->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "union tc main launch");
+    e = launch_tc_finalize((const uint64_t*)(W + w.mbuf), (const int*)(W + w.mcnt), kTcMainCap, ix->num_sms, thr, B,
+                           K, mode == 0 ? out_ids : nullptr, mode == 0 ? out_scores : nullptr,
+                           mode == 1 ? out_keys : nullptr, (int*)(W + w.flags), (unsigned int*)(W + w.bar), st, gate);
+    if (e != cudaSuccess) return cuda_fail(e, "union tc finalize launch");
+    if (ix->prof) ix->prof_launches += 3;
+  }
   // 2. one ring-scan launch for every user, starting from the thresholds
   const size_t uoff = align256(w.end);
   const WsLayout wl = ws_layout(pl, B, K);
@@ -707,6 +734,10 @@ int search_union(linr_index* ix, const void* q, int B, int V, const linr_clause*
   sp.wmask = wmask;
   sp.ring = pl.ring;
   sp.init_thr = thr;
+  sp.gate = gate;
+  sp.gate_want = 0;
+  mp.gate = gate;
+  mp.gate_want = 0;
   sp.mp = mp;
   e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, sp, pl.grid, pl.smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "union scan launch");

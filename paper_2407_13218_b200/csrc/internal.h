@@ -52,6 +52,8 @@ struct MergeParams {
   int bucket_sort;               // 1: skip the sorted-prefix merge (bucket sort; A/B knob LINR_MERGE_BUCKET)
   const uint64_t* thr;           // [B] thresholds the scan started from (union path), or null
   int* flags;                    // [B] set to 1 when fewer than K keys >= thr[u] were found (recompute)
+  const int* gate;               // merge_kernel: run only if *gate == gate_want (null: always)
+  int gate_want;
   unsigned long long* dbg;       // diagnostics timers
 };
 
@@ -80,6 +82,8 @@ struct ScanParams {
   int fuse_merge;                // 1: the last nu CTAs run the merge (mp) for this launch's users
   int ring;                      // > 0: warp-specialised scan with this many row-group slots
   const uint64_t* init_thr;      // [nu] starting CTA thresholds (union path: sample-derived), or null
+  const int* gate;               // non-null: run only if *gate == gate_want (device-side path choice)
+  int gate_want;
   MergeParams mp;                // merge of this launch's users (user index relative to the launch)
   int ncl[8];
   KClause cl[8][16];
@@ -139,6 +143,8 @@ struct TcParams {
   int sample_tiles;      // sample pass: tiles per CTA (0 = main pass, all tiles)
   int dyn;               // 1: epilogue warps of a TMEM lane quarter take chunks dynamically
   int sample_thr;        // 1: tiles spread like the sample pass, main-pass epilogue (keys >= thr)
+  const int* gate;       // non-null: run only if *gate == gate_want (device-side path choice)
+  int gate_want;
   unsigned long long* dbg;   // diagnostics: per-tile role timestamps of CTA 0 (null = off)
 };
 
@@ -149,9 +155,11 @@ bool tc_encode_map(CUtensorMap* m, const void* base, int64_t rows, int rowbytes,
 cudaError_t launch_tc_scan(int dtype, int dim, int np, const TcParams& p, int grid, cudaStream_t st);
 cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap, int grid, int nu, int K,
                                 int sample_items, const DevHeader* hdr, uint64_t* thr, cudaStream_t st, const uint64_t* floor = nullptr);
+cudaError_t launch_tc_decide(const uint64_t* thr, const int* scnt, int grid, int64_t sample_rows, const DevHeader* hdr,
+                             int nu, int* gate, cudaStream_t st);
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
-                               unsigned int* fb_bar, cudaStream_t st);
+                               unsigned int* fb_bar, cudaStream_t st, const int* gate = nullptr);
 cudaError_t launch_tc_count(const uint64_t* attr, int64_t cap_pad, const uint32_t* live, const DevHeader* hdr,
                             const KClause* cl, const int* ncl, int nu, unsigned long long* counts, int grid,
                             cudaStream_t st);

@@ -11,6 +11,7 @@ __global__ void __launch_bounds__(kMergeNT, 1) merge_kernel(const __grid_constan
   // launched as a programmatic dependent of the scan: wait until the scan grid has completed and
   // its results are visible (a no-op for an ordinary launch)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.gate != nullptr && *(volatile const int*)p.gate != p.gate_want) return;   // path not chosen
   merge_user<kMergeNT>(p, blockIdx.x, smem_raw);
 }
 

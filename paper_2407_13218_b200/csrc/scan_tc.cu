@@ -336,6 +336,7 @@ LINR_DEV bool tc_clauses_reg(const uint4* k, int maxc, uint64_t w0, bool one, co
 // them, lane j taking column j: exact key >= T_u, clauses, append.
 template <int DT, int D, int NP>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(const __grid_constant__ TcParams p) {
+  if (p.gate != nullptr && *(volatile const int*)p.gate != p.gate_want) return;   // path not chosen
   using G = TcGeom<DT, D>;
   constexpr bool kInt = DT == LINR_I8;
   constexpr int NEPI = kTcThreads - 128;   // epilogue threads (warps 4..)
@@ -841,7 +842,8 @@ struct FinSmem {
 __global__ void __launch_bounds__(512, 1) tc_finalize_kernel(const uint64_t* buf, const int* cnt, int cap, int grid,
                                                              const uint64_t* thr, int K, int64_t* out_ids,
                                                              float* out_scores, uint64_t* out_keys, int* flags,
-                                                             unsigned int* fb_bar, int room) {
+                                                             unsigned int* fb_bar, int room, const int* gate) {
+  if (gate != nullptr && *(volatile const int*)gate != 1) return;   // union path chosen instead
   extern __shared__ __align__(16) unsigned char fsm[];
   FinSmem* f = reinterpret_cast<FinSmem*>(fsm);
   uint64_t* s = reinterpret_cast<uint64_t*>(fsm + ((sizeof(FinSmem) + 15) & ~size_t(15)));
@@ -1046,16 +1048,41 @@ cudaError_t launch_tc_threshold(const uint64_t* sbuf, const int* scnt, int scap,
   return cudaGetLastError();
 }
 
+// Device-side choice for small batches (union path): 1 = every user has a sample threshold (the
+// dense tcgen05 pass wins), 0 = some user has none (low pass rate: the union scan wins).
+// The dense pass tests every (row, user) pair against T_u BEFORE the clauses, so its hot pairs grow
+// as 1 / pass rate: it is chosen only when every user has a threshold AND passes >= 1/25 of the
+// sampled rows (c2 B = 8: HIGH 11.7 % -> tcgen05 0.44 ms; LOW 0.24 % -> union 0.20 ms).
+__global__ void tc_decide_kernel(const uint64_t* thr, const int* scnt, int grid, int64_t sample_rows,
+                                 const DevHeader* hdr, int nu, int* gate) {
+  const int u = threadIdx.x;
+  bool ok = true;
+  if (u < nu) {
+    long long passed = 0;
+    for (int c = 0; c < grid; ++c) passed += scnt[(size_t)u * grid + c];
+    const int64_t hwm = (int64_t)(*(volatile const unsigned long long*)&hdr->hwm);
+    const int64_t rows = sample_rows < hwm ? sample_rows : hwm;
+    ok = thr[u] != 0ull && passed * 25 >= rows;
+  }
+  const int all = __syncthreads_and(ok);
+  if (u == 0) *gate = all ? 1 : 0;
+}
+cudaError_t launch_tc_decide(const uint64_t* thr, const int* scnt, int grid, int64_t sample_rows, const DevHeader* hdr,
+                             int nu, int* gate, cudaStream_t st) {
+  tc_decide_kernel<<<1, 256, 0, st>>>(thr, scnt, grid, sample_rows, hdr, nu, gate);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tc_finalize(const uint64_t* buf, const int* cnt, int cap, int grid, const uint64_t* thr, int nu,
                                int K, int64_t* out_ids, float* out_scores, uint64_t* out_keys, int* flags,
-                               unsigned int* fb_bar, cudaStream_t st) {
+                               unsigned int* fb_bar, cudaStream_t st, const int* gate) {
   const size_t smem = ((sizeof(FinSmem) + 15) & ~size_t(15)) + (size_t)(kTcFinCap + 4096) * 8;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(tc_finalize_kernel), smem);
   if (e != cudaSuccess) return e;
   // LINR_TC_FIN_ROOM (test knob): a smaller gather room forces the exact global-memory selection
   const int room = std::max(K, std::min(kTcFinCap, env_int("LINR_TC_FIN_ROOM", kTcFinCap)));
   tc_finalize_kernel<<<nu, 512, smem, st>>>(buf, cnt, cap, grid, thr, K, out_ids, out_scores, out_keys, flags,
-                                            fb_bar, room);
+                                            fb_bar, room, gate);
   return cudaGetLastError();
 }
 

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(WsGeom<DT, D>::NT, 1) scan_ws_kernel(const __g
   constexpr int NT = W::NT, NPW = W::NPW, NCW = W::NCW, NU = NQV;
   constexpr bool kInt = (DT == LINR_I8);
   using acc_t = typename std::conditional<kInt, int, float>::type;
+  if (p.gate != nullptr && *(volatile const int*)p.gate != p.gate_want) return;   // path not chosen
   // programmatic dependent launch: the merge kernel queued behind this scan may be scheduled now
   // (it waits in griddepcontrol.wait for this grid to complete and its writes to be visible)
   asm volatile("griddepcontrol.launch_dependents;");

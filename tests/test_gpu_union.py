@@ -130,3 +130,23 @@ def test_small_batch_without_pass_counts_takes_tcgen05(monkeypatch, B, V):
     ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, (ids, sc, torch.from_numpy(ref[2])), ref, True,
           what=f"tc no-pass B{B} V{V}")
+
+
+@pytest.mark.parametrize("preset", ["HIGH", "LOW", "ALL"])
+def test_union_gate_device_choice(preset):
+    """B*V >= 7 without pass counts: the union path launches both the dense tcgen05 pass and the
+    union scan behind a device-side gate (every user has a sample threshold -> tcgen05); whichever
+    runs, the result is the oracle's (8 launches: sample, threshold, decide, tc main, finalize,
+    union scan, merge, fallback)."""
+    dtype, d, n, K, B = dg.I8, 128, 300_000, 700, 8
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_DENSE)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype, dg.MODE_DENSE)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    ids, sc, _ = ix.search(to_torch(Q, dtype, DEV), cls, K, want_pass=False)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 8
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, (ids, sc, torch.from_numpy(ref[2])), ref, True,
+          what=f"union gate {preset}")

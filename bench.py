@@ -301,8 +301,12 @@ def run_gpu(args):
     # pass counts are not part of the paper's result (reading R24): requested only where they are
     # free (one user: the fused scan counts its passers) or asked for
     want_pass = args.batch == 1 or args.pass_counts
-    tc_route = args.batch * args.vectors >= 9 or (args.batch * args.vectors >= 7 and not want_pass
-                                                   and os.environ.get("LINR_TC_NOPASS") == "1")
+    # the dense tcgen05 roofline applies where that path always runs; 3 <= B <= 16 (V = 1) without
+    # pass counts take the union path, whose device-side gate picks the dense pass or the union
+    # scans -- their algorithmic bytes are the attribute stream plus the union of passing rows
+    union_route = args.vectors == 1 and 3 <= args.batch <= 16 and not want_pass
+    tc_route = (args.batch * args.vectors >= 9 and not union_route) or (
+        args.batch * args.vectors >= 7 and not want_pass and os.environ.get("LINR_TC_NOPASS") == "1")
 
     def step():
         if sidx is not None:
@@ -485,7 +489,7 @@ def run_gpu(args):
     scan_ms = prof["scan_ms"] / max(1, prof["searches"])
     peak, peak_src = measured_peaks()
     roof = None
-    if 1 < args.batch <= 8 and not tc_route:
+    if 1 < args.batch <= 16 and not tc_route:
         # GEMV path with several users: the algorithmic bytes of the step are one read of the
         # attribute words + liveness bits and the rows that pass for at least one user (union)
         a = ix.attr_storage.view(torch.int64)[:n_local]

@@ -559,7 +559,9 @@ int validate_query(const linr_index* ix, const void* q, int B, int V, const linr
 bool union_ok(const linr_index* ix, int B, int V, int maxc, int wmax) {
   // measured (profiles/r02w): B = 8 HIGH 0.56 vs 0.62 ms per-user, ALL 0.58 vs 3.9 ms, LOW 0.20 vs
   // 0.38 ms; B = 4 equal at HIGH; B = 2 and V > 1 (the consumers' V-max path) slower -> per user
-  if (V != 1 || B < 3 || B > 8 || B > kMaxUsers || env_int("LINR_UNION", 1) == 0) return false;
+  // B in [9, 16] (two ring-scan launches of <= 8 users) only behind the device-side gate, i.e.
+  // without pass counts (search_impl)
+  if (V != 1 || B < 3 || B > 16 || env_int("LINR_UNION", 1) == 0) return false;
   if (std::getenv("LINR_NO_WS") || std::getenv("LINR_MAX_NU")) return false;   // kernel-variant knobs
   return tc_supported(ix->d.dtype, ix->d.dim, B * V, V) &&
          tc_smem_bytes(ix->d.dtype, ix->d.dim, tc_np(B * V), B, maxc, wmax) <= (size_t)ix->smem_optin;
@@ -568,7 +570,7 @@ size_t union_ws_bytes(const linr_index* ix, int B, int V, int K, Plan* pl) {
   std::string why;
   TcWs w;
   if (!tc_layout(ix, B, V, K, &w, &why)) return 0;
-  if (!make_plan(ix, B, V, K, pl, &why, false, B)) return 0;
+  if (!make_plan(ix, B, V, K, pl, &why, false, std::min(B, kMaxUsers))) return 0;
   return align256(w.end) + ws_layout(*pl, B, K).end;
 }
 
@@ -700,47 +702,54 @@ int search_union(linr_index* ix, const void* q, int B, int V, const linr_clause*
   mp.thr = thr;
   mp.flags = (int*)(W + w.flags);
   mp.dbg = debug_buffer();
-  ScanParams sp;
-  std::memset(&sp, 0, sizeof(sp));
-  sp.emb = ix->emb;
-  sp.attr = ix->attr;
-  sp.live = ix->live;
-  sp.hdr = ix->hdr;
-  sp.cap_pad = ix->cap_pad;
-  sp.row0 = (uint32_t)ix->d.global_row0;
-  sp.nu = B;
-  sp.V = V;
-  sp.K = K;
-  sp.C = pl.C;
-  sp.bufcap = pl.bufcap;
-  sp.list_cap = pl.list_cap;
-  sp.dbg = debug_buffer();
-  sp.q = q;
-  sp.out_samp = samp;
-  sp.out_list = lists;
-  sp.out_cnt = cnts;
-  sp.out_pass = pass;
-  uint32_t wmask = 0;
-  for (int b = 0; b < B; ++b) {
-    sp.ncl[b] = off[b + 1] - off[b];
-    for (int c = 0; c < sp.ncl[b]; ++c) {
-      const linr_clause& k = cl[off[b] + c];
-      sp.cl[b][c].mask = k.mask;
-      sp.cl[b][c].word = k.word;
-      sp.cl[b][c].rev = k.reverse;
-      wmask |= 1u << k.word;
-    }
-  }
-  sp.wmask = wmask;
-  sp.ring = pl.ring;
-  sp.init_thr = thr;
-  sp.gate = gate;
-  sp.gate_want = 0;
   mp.gate = gate;
   mp.gate_want = 0;
-  sp.mp = mp;
-  e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, sp, pl.grid, pl.smem, st);
-  if (e != cudaSuccess) return cuda_fail(e, "union scan launch");
+  // one ring-scan launch per group of <= kMaxUsers users (one launch for B <= 8)
+  for (int u0 = 0; u0 < B; u0 += pl.nu_g) {
+    const int nu = std::min(pl.nu_g, B - u0);
+    ScanParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.emb = ix->emb;
+    sp.attr = ix->attr;
+    sp.live = ix->live;
+    sp.hdr = ix->hdr;
+    sp.cap_pad = ix->cap_pad;
+    sp.row0 = (uint32_t)ix->d.global_row0;
+    sp.nu = nu;
+    sp.V = V;
+    sp.K = K;
+    sp.C = pl.C;
+    sp.bufcap = pl.bufcap;
+    sp.list_cap = pl.list_cap;
+    sp.dbg = debug_buffer();
+    sp.q = (const char*)q + (size_t)u0 * V * ix->rowbytes;
+    const size_t part0 = (size_t)u0 * pl.grid;
+    sp.out_samp = samp + part0 * kScanSample;
+    sp.out_list = lists + part0 * pl.list_cap;
+    sp.out_cnt = cnts + part0;
+    sp.out_pass = pass + part0;
+    uint32_t wmask = 0;
+    for (int u = 0; u < nu; ++u) {
+      const int b = u0 + u;
+      sp.ncl[u] = off[b + 1] - off[b];
+      for (int c = 0; c < sp.ncl[u]; ++c) {
+        const linr_clause& k = cl[off[b] + c];
+        sp.cl[u][c].mask = k.mask;
+        sp.cl[u][c].word = k.word;
+        sp.cl[u][c].rev = k.reverse;
+        wmask |= 1u << k.word;
+      }
+    }
+    sp.wmask = wmask;
+    sp.ring = pl.ring;
+    sp.init_thr = thr + u0;
+    sp.gate = gate;
+    sp.gate_want = 0;
+    sp.mp = mp;
+    e = launch_scan_gemv(ix->d.dtype, ix->d.dim, pl.nqv, sp, pl.grid, pl.smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "union scan launch");
+    if (ix->prof && u0 > 0) ix->prof_launches += 1;
+  }
   if (ix->prof) cudaEventRecord(pe.e1, st);
   // 3. merge (flags users with fewer than K keys >= T_u), 4. exact recomputation of flagged users
   e = launch_merge(mp, B, st, false);
@@ -793,12 +802,20 @@ int search_impl(linr_index* ix, const void* q, int B, int V, const linr_clause* 
   // vs 0.56 ms on the union path -- but at LOW every user's sample threshold is 0 and it takes
   // 1.36 ms vs 0.20 ms; the host cannot tell the two apart, so B*V <= 8 stays on the union path
   // unless LINR_TC_NOPASS=1; profiles/r02np)
+  if (!live_ovr && !ix->force_gemv && out_pass == nullptr && B * V >= 9 &&
+      union_ok(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
+    // 9 <= B <= 16 without pass counts: the union path with its device-side gate runs the dense
+    // tcgen05 pass at high pass rates and the union scans (two launches) at low ones
+    Plan up;
+    if (union_ws_bytes(ix, B, V, K, &up) > 0)
+      return search_union(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
+  }
   if (!live_ovr && !ix->force_gemv &&
       (use_tc(ix, B, V, max_clauses(off, B), max_word(cl, off, B)) ||
        (out_pass == nullptr && env_int("LINR_TC_NOPASS", 0) &&
         use_tc_nopass(ix, B, V, max_clauses(off, B), max_word(cl, off, B)))))
     return search_tc(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);
-  if (!live_ovr && !ix->force_gemv && union_ok(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
+  if (!live_ovr && !ix->force_gemv && B <= 8 && union_ok(ix, B, V, max_clauses(off, B), max_word(cl, off, B))) {
     Plan up;
     if (union_ws_bytes(ix, B, V, K, &up) > 0)
       return search_union(ix, q, B, V, cl, off, K, ws, ws_bytes, mode, out_ids, out_scores, out_keys, out_pass, st);

@@ -150,3 +150,21 @@ def test_union_gate_device_choice(preset):
     ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
     check(dtype, vals, attrs, np.ones(n), Q, cls, K, (ids, sc, torch.from_numpy(ref[2])), ref, True,
           what=f"union gate {preset}")
+
+
+@pytest.mark.parametrize("B,preset", [(16, "LOW"), (12, "HIGH"), (16, "ALL"), (9, "LOW")])
+def test_union_gate_two_groups(B, preset):
+    """9 <= B <= 16 without pass counts: union scans over two groups of <= 8 users (or the dense
+    tcgen05 pass, chosen on the device); exact either way."""
+    dtype, d, n, K = dg.I8, 64, 250_000, 600
+    vals, attrs = dg.gen_items(dg.DATA_SEED, 0, n, d, dtype, dg.MODE_DENSE)
+    ix = make_index(vals, attrs, dtype)
+    Q = dg.gen_queries(dg.QUERY_SEED, dg.DATA_SEED, n, B, 1, d, dtype, dg.MODE_DENSE)
+    cls = dg.gen_clauses(dg.QUERY_SEED, B, preset)
+    ix.profile(True)
+    ids, sc, _ = ix.search(to_torch(Q, dtype, DEV), cls, K, want_pass=False)
+    torch.cuda.synchronize()
+    assert ix.profile_read()["launches"] == 9
+    ref = oracle.search(dtype, vals, attrs, np.ones(n), Q, cls, K)
+    check(dtype, vals, attrs, np.ones(n), Q, cls, K, (ids, sc, torch.from_numpy(ref[2])), ref, True,
+          what=f"union two groups B{B} {preset}")
